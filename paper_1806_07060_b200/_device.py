@@ -1,0 +1,103 @@
+"""Device plumbing: operand staging, per-thread workspaces, streams.
+
+PyTorch provides CUDA memory and streams only; every GEMM runs in
+libadaptgemm_b200.so.  Host (numpy) operands are staged through pinned
+buffers into device tensors; device (torch.cuda) operands are used in place.
+"""
+
+import threading
+
+import numpy as np
+
+_torch = None
+
+
+def torch():
+    """Import torch lazily (the CPU-only parts of the package do not need it)."""
+    global _torch
+    if _torch is None:
+        import torch as _t
+        _torch = _t
+    return _torch
+
+
+class DeviceUnavailableError(RuntimeError):
+    """No CUDA device: the GEMM path has no CPU fallback."""
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise DeviceUnavailableError(
+            "no CUDA device visible: adaptgemm-b200 runs GEMMs only on the GPU (sm_100a)")
+    return t
+
+
+def is_device_tensor(x) -> bool:
+    t = _torch
+    if t is None:
+        # avoid importing torch just to answer "no" for numpy inputs
+        return type(x).__module__.startswith("torch")
+    return isinstance(x, t.Tensor)
+
+
+_NP_TO_CODE = {np.dtype(np.float32): 0, np.dtype(np.float64): 1}
+
+
+def dtype_code(dtype) -> int:
+    """0 float32, 1 float64, -1 anything else (numpy or torch dtype)."""
+    t = _torch
+    if t is not None and isinstance(dtype, t.dtype):
+        return {t.float32: 0, t.float64: 1}.get(dtype, -1)
+    try:
+        return _NP_TO_CODE.get(np.dtype(dtype), -1)
+    except TypeError:
+        return -1
+
+
+def row_major(t):
+    """A 2-D tensor whose last dim is contiguous (returns it or a copy)."""
+    if t.dim() == 2 and t.stride(1) == 1 and t.stride(0) >= max(1, t.shape[1]):
+        return t
+    return t.contiguous()
+
+
+def leading_dim(t) -> int:
+    return max(int(t.stride(0)), int(t.shape[1]), 1)
+
+
+_tls = threading.local()
+
+
+def workspace(nbytes: int, device):
+    """Per-thread, per-device grow-only byte buffer (allocation is never timed)."""
+    t = torch()
+    cache = getattr(_tls, "ws", None)
+    if cache is None:
+        cache = _tls.ws = {}
+    key = (device.type, device.index)
+    buf = cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        size = max(nbytes, 1 << 20)
+        if buf is not None:
+            size = max(size, buf.numel() * 2)
+        buf = t.empty(size, dtype=t.uint8, device=device)
+        cache[key] = buf
+    return buf
+
+
+def current_stream_handle(device) -> int:
+    t = torch()
+    return int(t.cuda.current_stream(device).cuda_stream)
+
+
+def to_device(a: np.ndarray, device):
+    """Copy a numpy matrix to a contiguous device tensor."""
+    t = torch()
+    src = t.from_numpy(np.ascontiguousarray(a))
+    return src.to(device=device, non_blocking=False)
+
+
+def default_device():
+    t = require_cuda()
+    return t.device("cuda", t.cuda.current_device())

@@ -1,0 +1,379 @@
+// abi.cu -- the C-ABI declared in include/adaptgemm_b200.h (GEMM side).
+//
+// Validation order follows gemm_execute (kernels.py:336-339): legality first
+// (ConfigError), then operands (ShapeError).  Timing follows tuner._measure
+// (tuner.py:139-158) with CUDA events on the caller's stream instead of
+// time.perf_counter around a host call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels.cuh"
+#include "launch.cuh"
+#include "registry.h"
+
+extern const ag::EntryTableFn g_entry_tables[];
+extern const int g_num_entry_tables;
+
+namespace {
+
+thread_local std::string t_err;
+
+int set_err(int code, const std::string& msg) {
+    t_err = msg;
+    return code;
+}
+
+uint64_t make_key(int family, int dtype, int bm, int bn, int bk, int tm, int tn, int uk) {
+    auto f = [](int v, int bits) -> uint64_t { return (uint64_t)(v & ((1 << bits) - 1)); };
+    return f(family, 4) | f(dtype, 2) << 4 | f(bm, 11) << 6 | f(bn, 11) << 17 | f(bk, 9) << 28 | f(tm, 6) << 37 |
+           f(tn, 6) << 43 | f(uk, 6) << 49;
+}
+
+struct Registry {
+    std::unordered_map<uint64_t, ag::LaunchFn> map;
+    int count = 0;
+};
+
+Registry& registry() {
+    static Registry* reg = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        reg = new Registry();
+        for (int t = 0; t < g_num_entry_tables; ++t) {
+            int n = 0;
+            const ag::KernelEntry* e = g_entry_tables[t](&n);
+            for (int i = 0; i < n; ++i) {
+                reg->map[make_key(e[i].family, e[i].dtype, e[i].bm, e[i].bn, e[i].bk, e[i].tm, e[i].tn, e[i].uk)] =
+                    e[i].fn;
+                reg->count++;
+            }
+        }
+    });
+    return *reg;
+}
+
+bool in_range(const ag_config& c) {
+    return c.bm > 0 && c.bn > 0 && c.bk > 0 && c.tm > 0 && c.tn > 0 && c.uk > 0 && c.bm < 2048 && c.bn < 2048 &&
+           c.bk < 512 && c.tm < 64 && c.tn < 64 && c.uk < 64;
+}
+
+// exact instantiation, else the run-time-tile kernel for (tm, tn)
+ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
+    if (!in_range(c)) return nullptr;
+    auto& m = registry().map;
+    auto it = m.find(make_key(c.family, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk));
+    if (it != m.end()) return it->second;
+    it = m.find(make_key(c.family, dtype, 0, 0, 0, c.tm, c.tn, 0));
+    if (it != m.end()) return it->second;
+    return nullptr;
+}
+
+std::string config_str(const ag_config& c) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "%s:%d-%d-%d-%d-%d-%d", c.family == AG_FAMILY_DIRECT ? "direct" : "indirect", c.bm, c.bn,
+             c.bk, c.tm, c.tn, c.uk);
+    return buf;
+}
+
+int check_operands(const ag_shape* s, int dtype, const void* A, int64_t lda, const void* B, int64_t ldb,
+                   const void* C, int64_t ldc, const void* out, int64_t ldo) {
+    if (!s) return set_err(AG_ERR_SHAPE, "null shape");
+    if (s->m < 1 || s->n < 1 || s->k < 1) return set_err(AG_ERR_SHAPE, "M, N, K must be positive");
+    if (dtype != AG_F32 && dtype != AG_F64) return set_err(AG_ERR_SHAPE, "unsupported dtype, want float32 or float64");
+    if (!A || !B || !C || !out) return set_err(AG_ERR_SHAPE, "null operand pointer");
+    if (lda < (s->trans_a ? s->m : s->k)) return set_err(AG_ERR_SHAPE, "lda too small for op(A)");
+    if (ldb < (s->trans_b ? s->k : s->n)) return set_err(AG_ERR_SHAPE, "ldb too small for op(B)");
+    if (ldc < s->n || ldo < s->n) return set_err(AG_ERR_SHAPE, "ldc/ldo too small");
+    if (s->m > 0x7fffffffLL || s->n > 0x7fffffffLL || s->k > 0x7fffffffLL)
+        return set_err(AG_ERR_SHAPE, "dimension exceeds 2^31-1");
+    return AG_OK;
+}
+
+ag::GemmCall make_call(const ag_shape* s, const ag_config* c, int dtype, const void* A, int64_t lda, const void* B,
+                       int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo, void* ws, size_t ws_bytes,
+                       void* stream) {
+    ag::GemmCall g;
+    g.M = s->m; g.N = s->n; g.K = s->k;
+    g.alpha = s->alpha; g.beta = s->beta;
+    g.ta = s->trans_a ? 1 : 0; g.tb = s->trans_b ? 1 : 0;
+    g.dtype = dtype;
+    g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc; g.out = out; g.ldo = ldo;
+    g.ws = ws; g.ws_bytes = ws_bytes;
+    g.stream = static_cast<cudaStream_t>(stream);
+    g.bm = c->bm; g.bn = c->bn; g.bk = c->bk; g.tm = c->tm; g.tn = c->tn; g.uk = c->uk;
+    g.err = &t_err;
+    return g;
+}
+
+// validate + resolve; on success *fn is the launcher
+int prepare(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A, int64_t lda,
+            const void* B, int64_t ldb, const void* C, int64_t ldc, const void* out, int64_t ldo, ag::LaunchFn* fn) {
+    if (!c) return set_err(AG_ERR_CONFIG, "null config");
+    if (caps && !ag_is_legal(c, caps)) return set_err(AG_ERR_CONFIG, "illegal config " + config_str(*c) + " for caps");
+    int r = check_operands(s, dtype, A, lda, B, ldb, C, ldc, out, ldo);
+    if (r) return r;
+    *fn = find_kernel(*c, dtype);
+    if (!*fn)
+        return set_err(AG_ERR_CONFIG, "no sm_100a kernel compiled for " + config_str(*c) +
+                                          (dtype == AG_F64 ? " (float64)" : " (float32)"));
+    return AG_OK;
+}
+
+__global__ void spin_kernel(long long ns) {
+    long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
+struct TimingRes {
+    cudaStream_t cap = nullptr;
+    std::vector<cudaEvent_t> ev;
+    ~TimingRes() {
+        // process teardown: the driver may be gone already; ignore errors
+    }
+    cudaEvent_t event(size_t i) {
+        while (ev.size() <= i) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+            ev.push_back(e);
+        }
+        return ev[i];
+    }
+    cudaStream_t capture_stream() {
+        if (!cap) cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+        return cap;
+    }
+};
+thread_local TimingRes t_res;
+
+double median_of(std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    const size_t n = v.size();
+    return (n % 2) ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+}
+
+int timed_run(const ag::GemmCall& call, ag::LaunchFn fn, int warmup, int repeats, int inner, double* median_s) {
+    if (repeats < 1) return set_err(AG_ERR_SHAPE, "repeats must be >= 1");
+    cudaStream_t st = call.stream;
+    // warmup runs (>= 1: also sets kernel attributes before graph capture)
+    for (int w = 0; w < std::max(warmup, 1); ++w) {
+        int r = fn(call);
+        if (r) return r;
+    }
+    cudaEvent_t e0 = t_res.event(0), e1 = t_res.event(1);
+    if (!e0 || !e1) return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
+    if (inner <= 0) {
+        spin_kernel<<<1, 1, 0, st>>>(20000);
+        cudaEventRecord(e0, st);
+        int r = fn(call);
+        if (r) return r;
+        cudaEventRecord(e1, st);
+        if (cudaEventSynchronize(e1) != cudaSuccess) return set_err(AG_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double target_ms = 0.05;
+        inner = (int)std::ceil(target_ms / std::max((double)ms, 1e-4));
+        inner = std::min(std::max(inner, 1), 64);
+    }
+    // capture `inner` back-to-back paths into one graph
+    cudaStream_t cap = t_res.capture_stream();
+    if (!cap) return set_err(AG_ERR_CUDA, "cannot create capture stream");
+    ag::GemmCall cc = call;
+    cc.stream = cap;
+    if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return set_err(AG_ERR_CUDA, "cudaStreamBeginCapture failed");
+    int rr = AG_OK;
+    for (int i = 0; i < inner && rr == AG_OK; ++i) rr = fn(cc);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+    if (rr) {
+        if (graph) cudaGraphDestroy(graph);
+        return rr;
+    }
+    if (ce != cudaSuccess || !graph) return set_err(AG_ERR_CUDA, std::string("graph capture failed: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t exec = nullptr;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return set_err(AG_ERR_CUDA, std::string("graph instantiate failed: ") + cudaGetErrorString(ce));
+    // back the queue up so no sample includes host enqueue gaps
+    spin_kernel<<<1, 1, 0, st>>>(20000 + 4000LL * repeats);
+    for (int r = 0; r < repeats; ++r) {
+        cudaEvent_t a = t_res.event(2 + 2 * r), b = t_res.event(3 + 2 * r);
+        if (!a || !b) {
+            cudaGraphExecDestroy(exec);
+            return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
+        }
+        cudaEventRecord(a, st);
+        cudaGraphLaunch(exec, st);
+        cudaEventRecord(b, st);
+    }
+    ce = cudaStreamSynchronize(st);
+    cudaGraphExecDestroy(exec);
+    if (ce != cudaSuccess) return set_err(AG_ERR_CUDA, std::string("kernel failed: ") + cudaGetErrorString(ce));
+    std::vector<double> samples(repeats);
+    for (int r = 0; r < repeats; ++r) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t_res.ev[2 + 2 * r], t_res.ev[3 + 2 * r]);
+        samples[r] = (double)ms * 1e-3 / inner;
+    }
+    *median_s = std::max(median_of(samples), 1e-9);
+    return AG_OK;
+}
+
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float b, float c) {
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-7f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) a[i] = __fmaf_rn(a[i], b, c);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += a[i];
+    if (s == 1234.5f) out[0] = s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ag_last_error(void) { return t_err.c_str(); }
+const char* ag_version(void) { return "adaptgemm-b200 0.1.0 (sm_100a)"; }
+
+int ag_is_legal(const ag_config* c, const ag_caps* caps) {
+    if (!c || !caps) return 0;
+    if (std::min({c->bm, c->bn, c->bk, c->tm, c->tn, c->uk}) < 1) return 0;
+    if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT) return 0;
+    if (c->family == AG_FAMILY_DIRECT && c->uk != 1) return 0;
+    if (c->bm % c->tm || c->bn % c->tn || c->bk % c->uk) return 0;
+    const int64_t cap = c->family == AG_FAMILY_DIRECT ? caps->register_tile_cap_direct : caps->register_tile_cap_indirect;
+    if ((int64_t)c->tm * c->tn > cap) return 0;
+    if ((int64_t)(c->bm + c->bn) * c->bk * caps->element_size > caps->tile_memory_cap) return 0;
+    const int64_t max_threads = caps->max_threads > 0 ? caps->max_threads : 1024;
+    const int64_t threads = (int64_t)(c->bm / c->tm) * (c->bn / c->tn);
+    if (threads > max_threads) return 0;
+    // register file: accumulators + fragments + ~24 addressing registers
+    if (threads * ((int64_t)c->tm * c->tn + c->tm + c->tn + 24) > 65536) return 0;
+    return 1;
+}
+
+int ag_has_kernel(const ag_config* c, int dtype) { return c && find_kernel(*c, dtype) != nullptr; }
+
+int ag_num_kernels(void) { return registry().count; }
+
+size_t ag_workspace_bytes(const ag_shape* s, const ag_config* c, int dtype) {
+    if (!s || !c || c->family != AG_FAMILY_INDIRECT || !in_range(*c)) return 0;
+    if (dtype == AG_F64) return ag::indirect_workspace_bytes<double>(s->m, s->n, s->k, c->bm, c->bn, c->bk);
+    return ag::indirect_workspace_bytes<float>(s->m, s->n, s->k, c->bm, c->bn, c->bk);
+}
+
+int ag_gemm(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A, int64_t lda,
+            const void* B, int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo, void* ws, size_t ws_bytes,
+            void* stream) {
+    ag::LaunchFn fn = nullptr;
+    int r = prepare(s, c, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, &fn);
+    if (r) return r;
+    return fn(make_call(s, c, dtype, A, lda, B, ldb, C, ldc, out, ldo, ws, ws_bytes, stream));
+}
+
+int ag_gemm_timed(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A, int64_t lda,
+                  const void* B, int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo, void* ws,
+                  size_t ws_bytes, void* stream, int warmup, int repeats, int inner, double* median_s) {
+    ag::LaunchFn fn = nullptr;
+    int r = prepare(s, c, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, &fn);
+    if (r) return r;
+    if (!median_s) return set_err(AG_ERR_SHAPE, "null median_s");
+    return timed_run(make_call(s, c, dtype, A, lda, B, ldb, C, ldc, out, ldo, ws, ws_bytes, stream), fn, warmup,
+                     repeats, inner, median_s);
+}
+
+int ag_tune(const ag_shape* s, const ag_config* configs, int n_configs, const ag_caps* caps, int dtype, const void* A,
+            int64_t lda, const void* B, int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo, void* ws,
+            size_t ws_bytes, void* stream, int warmup, int repeats, double* elapsed_s, int* failed_index) {
+    if (failed_index) *failed_index = -1;
+    for (int i = 0; i < n_configs; ++i) {
+        int r = ag_gemm_timed(s, &configs[i], caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, ws, ws_bytes, stream,
+                              warmup, repeats, 0, &elapsed_s[i]);
+        if (r) {
+            if (failed_index) *failed_index = i;
+            t_err = "config " + config_str(configs[i]) + ": " + t_err;
+            return r;
+        }
+    }
+    return AG_OK;
+}
+
+int ag_gemm_reference(const ag_shape* s, int dtype, const void* A, int64_t lda, const void* B, int64_t ldb,
+                      const void* C, int64_t ldc, void* out, int64_t ldo, void* stream) {
+    int r = check_operands(s, dtype, A, lda, B, ldb, C, ldc, out, ldo);
+    if (r) return r;
+    if (s->m > 65535) return set_err(AG_ERR_SHAPE, "gemm_reference supports M <= 65535");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    dim3 grid((unsigned)((s->n + 255) / 256), (unsigned)s->m);
+    if (dtype == AG_F32)
+        ag::reference_gemm_kernel<float><<<grid, 256, 0, st>>>(
+            (int)s->m, (int)s->n, (int)s->k, s->alpha, s->beta, s->trans_a, s->trans_b, (const float*)A, lda,
+            (const float*)B, ldb, (const float*)C, ldc, (float*)out, ldo);
+    else
+        ag::reference_gemm_kernel<double><<<grid, 256, 0, st>>>(
+            (int)s->m, (int)s->n, (int)s->k, s->alpha, s->beta, s->trans_a, s->trans_b, (const double*)A, lda,
+            (const double*)B, ldb, (const double*)C, ldc, (double*)out, ldo);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? AG_OK : set_err(AG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int ag_pack_padded(int dtype, const void* src, int64_t ld_src, int64_t rows, int64_t cols, int transpose, void* dst,
+                   int64_t pad_rows, int64_t pad_cols, void* stream) {
+    if (!src || !dst || rows < 0 || cols < 0 || pad_rows < rows || pad_cols < cols)
+        return set_err(AG_ERR_SHAPE, "bad pack_padded arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int r = dtype == AG_F64 ? ag::launch_pack<double>((double*)dst, pad_cols, pad_rows, pad_cols, (const double*)src,
+                                                      ld_src, rows, cols, transpose, st)
+                            : ag::launch_pack<float>((float*)dst, pad_cols, pad_rows, pad_cols, (const float*)src,
+                                                     ld_src, rows, cols, transpose, st);
+    return r ? set_err(r, "pack_padded launch failed") : AG_OK;
+}
+
+int ag_ffma_peak(void* stream, double* tflops) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    float* out = nullptr;
+    if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return set_err(AG_ERR_CUDA, "cudaMalloc failed");
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    ffma_peak_kernel<<<blocks, threads, 0, st>>>(out, 64, 1.000001f, 1e-7f);  // warm
+    cudaEvent_t e0 = t_res.event(0), e1 = t_res.event(1);
+    double best = 0.0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0, st);
+        ffma_peak_kernel<<<blocks, threads, 0, st>>>(out, iters, 1.000001f, 1e-7f);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double flops = 2.0 * 16 * 8 * (double)iters * blocks * threads;
+        best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    cudaError_t e = cudaGetLastError();
+    cudaFree(out);
+    if (e != cudaSuccess) return set_err(AG_ERR_CUDA, cudaGetErrorString(e));
+    *tflops = best;
+    return AG_OK;
+}
+
+}  // extern "C"

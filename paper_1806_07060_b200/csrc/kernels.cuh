@@ -1,0 +1,440 @@
+// kernels.cuh -- sm_100a CUDA kernels of the two GEMM families.
+//
+// Reference semantics (/root/reference/pkg/src/adaptgemm/kernels.py):
+//   direct   (_kernel_direct, :198-227): one kernel over the caller's unpadded
+//            operands; ragged tile edges and both transposes handled inside
+//            the kernel; always reads C (beta * C even when beta == 0).
+//   indirect (_run_indirect + pack_padded + _kernel_tiled, :230-260,
+//            :304-325): O(n^2) helper passes copy op(A), op(B) into zero-padded
+//            tile-multiple buffers, then a branch-free blocked core runs on
+//            exact multiples; C is only read when beta != 0 (:318-321).
+//
+// B200 design (not a translation of the numba loop nests):
+//   * block_m x block_n is the CTA tile, block_k the K depth of one shared
+//     memory stage, tile_m x tile_n the per-thread register tile, unroll_k the
+//     number of K steps whose fragments are loaded before the FMAs.
+//   * FP32 runs on the CUDA cores (FFMA) with fp32 accumulation; operands are
+//     staged global->shared with cp.async (16-byte, L1-bypassing, multi-stage
+//     ring for the indirect core; 4/8-byte zero-filling predicated copies for
+//     the direct family), register tiles read with 64/128-bit LDS in an
+//     interleaved layout that is bank-conflict free.
+//   * The indirect pack writes op(A)^T (K-major) so both operands stream as
+//     contiguous rows; the padded output + unpad copy of the reference are
+//     fused into a masked store epilogue (same values, two fewer passes).
+//   * BM/BN/BK == 0 instantiations take the tile sizes at run time (used for
+//     float64 and for legal configs outside the enumerated domains).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ag {
+
+typedef long long i64;
+
+template <typename T> struct VecW;
+template <> struct VecW<float> { static constexpr int W = 4; };
+template <> struct VecW<double> { static constexpr int W = 2; };
+
+// widest vector (elements) that divides n, bounded by 16 bytes
+template <typename T, int n> struct FragW {
+    static constexpr int W = (n % VecW<T>::W == 0) ? VecW<T>::W : ((n % 2 == 0 && VecW<T>::W >= 2) ? 2 : 1);
+};
+
+template <typename T, int W> struct alignas(sizeof(T) * W) Vec { T v[W]; };
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// cp.async with zero fill: copies `pred ? BYTES : 0` bytes, zero-fills the rest
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool pred = true) {
+    const uint32_t s = smem_addr(smem);
+    const int src = pred ? BYTES : 0;
+    if constexpr (BYTES == 16) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src) : "memory");
+    } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem), "n"(BYTES), "r"(src) : "memory");
+    }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ float fmadd(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fmadd(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// Interleaved register-tile layout: thread t (of TT along a dimension) owns
+// elements g*TT*W + t*W + e for g < TILE/W, e < W.  Consecutive threads read
+// consecutive W-vectors, so a warp's LDS.64/LDS.128 phases are conflict free.
+template <int W>
+__device__ __forceinline__ int tile_index(int i, int t, int TT) {
+    return (i / W) * TT * W + t * W + (i % W);
+}
+
+template <typename T, int TILE, int W>
+__device__ __forceinline__ void load_frag(T (&f)[TILE], const T* row, int t, int TT) {
+#pragma unroll
+    for (int g = 0; g < TILE / W; ++g) {
+        const Vec<T, W> v = *reinterpret_cast<const Vec<T, W>*>(row + g * TT * W + t * W);
+#pragma unroll
+        for (int e = 0; e < W; ++e) f[g * W + e] = v.v[e];
+    }
+}
+
+template <typename T>
+struct DirectParams {
+    int M, N, K;
+    T alpha, beta;
+    int ta, tb;
+    const T* A; i64 lda;
+    const T* B; i64 ldb;
+    const T* C; i64 ldc;
+    T* out; i64 ldo;
+    int bm, bn, bk;  // run-time tile sizes when the template sizes are 0
+};
+
+template <typename T>
+struct TiledParams {
+    int Mp, Np, Kp, M, N;
+    T alpha, beta;
+    int use_c;    // beta != 0: read C (reference packs C only then)
+    int vec_out;  // out/C rows are W-aligned: vector epilogue allowed
+    const T* At; i64 lda;  // Kp x Mp, op(A)^T, K-major, zero padded
+    const T* Bp; i64 ldb;  // Kp x Np, op(B), zero padded
+    const T* C; i64 ldc;
+    T* out; i64 ldo;
+    int bm, bn, bk, uk;
+};
+
+// thread bound of a kernel instantiation: exact for fixed tiles; for the
+// run-time-tile kernels sized so the register tile never spills
+template <typename T, int BM, int BN, int TM, int TN>
+__host__ __device__ constexpr int cta_threads_bound() {
+    return (BM > 0 && BN > 0) ? (BM / TM) * (BN / TN)
+         : ((int)(TM * TN * sizeof(T) / 4) >= 32 ? 256 : ((int)(TM * TN * sizeof(T) / 4) >= 16 ? 512 : 1024));
+}
+
+// shared-memory footprint helpers (host + device)
+template <typename T>
+__host__ __device__ constexpr int direct_pad() { return VecW<T>::W; }
+
+template <typename T>
+__host__ __device__ inline size_t direct_smem_bytes(int bm, int bn, int bk) {
+    return (size_t)2 * bk * ((bm + direct_pad<T>()) + (bn + direct_pad<T>())) * sizeof(T);
+}
+template <typename T>
+__host__ __device__ inline size_t tiled_smem_bytes(int bm, int bn, int bk, int stages) {
+    return (size_t)stages * bk * (bm + bn) * sizeof(T);
+}
+// pipeline depth of the indirect core: deep rings for small stages, capped
+// so that one CTA fits the 227 KB shared memory of an sm_100 SM
+template <typename T>
+__host__ __device__ constexpr int tiled_stages(int bm, int bn, int bk) {
+    return (bm == 0) ? 2
+         : ((size_t)4 * bk * (bm + bn) * sizeof(T) <= 96 * 1024 ? 4
+         : ((size_t)3 * bk * (bm + bn) * sizeof(T) <= 200 * 1024 ? 3 : 2));
+}
+
+// ---------------------------------------------------------------------------
+// direct family
+// ---------------------------------------------------------------------------
+template <typename T, int BM_, int BN_, int BK_, int TM, int TN>
+__global__ void __launch_bounds__(cta_threads_bound<T, BM_, BN_, TM, TN>())
+direct_gemm_kernel(const DirectParams<T> p) {
+    constexpr int PAD = direct_pad<T>();
+    constexpr int WA = FragW<T, TM>::W;
+    constexpr int WB = FragW<T, TN>::W;
+    const int BM = BM_ > 0 ? BM_ : p.bm;
+    const int BN = BN_ > 0 ? BN_ : p.bn;
+    const int BK = BK_ > 0 ? BK_ : p.bk;
+    const int TX = BN / TN, TY = BM / TM, NT = TX * TY;
+    const int LA = BM + PAD, LB = BN + PAD;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* As = reinterpret_cast<T*>(smem_raw);
+    T* Bs = As + 2 * BK * LA;
+
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int M = p.M, N = p.N, K = p.K;
+
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+    auto load_tile = [&](int kt, int s) {
+        const int k0 = kt * BK;
+        T* as = As + s * BK * LA;
+        T* bs = Bs + s * BK * LB;
+        if (!p.ta) {  // A is M x K: walk k fastest (contiguous in global)
+            for (int e = tid; e < BM * BK; e += NT) {
+                const int k = e % BK, i = e / BK;
+                const int gm = m0 + i, gk = k0 + k;
+                const bool ok = gm < M && gk < K;
+                const T* src = ok ? p.A + (i64)gm * p.lda + gk : p.A;
+                cp_async<sizeof(T)>(as + k * LA + i, src, ok);
+            }
+        } else {  // A stored K x M: walk m fastest
+            for (int e = tid; e < BM * BK; e += NT) {
+                const int i = e % BM, k = e / BM;
+                const int gm = m0 + i, gk = k0 + k;
+                const bool ok = gm < M && gk < K;
+                const T* src = ok ? p.A + (i64)gk * p.lda + gm : p.A;
+                cp_async<sizeof(T)>(as + k * LA + i, src, ok);
+            }
+        }
+        if (!p.tb) {  // B is K x N
+            for (int e = tid; e < BK * BN; e += NT) {
+                const int n = e % BN, k = e / BN;
+                const int gn = n0 + n, gk = k0 + k;
+                const bool ok = gn < N && gk < K;
+                const T* src = ok ? p.B + (i64)gk * p.ldb + gn : p.B;
+                cp_async<sizeof(T)>(bs + k * LB + n, src, ok);
+            }
+        } else {  // B stored N x K
+            for (int e = tid; e < BK * BN; e += NT) {
+                const int k = e % BK, n = e / BK;
+                const int gn = n0 + n, gk = k0 + k;
+                const bool ok = gn < N && gk < K;
+                const T* src = ok ? p.B + (i64)gn * p.ldb + gk : p.B;
+                cp_async<sizeof(T)>(bs + k * LB + n, src, ok);
+            }
+        }
+    };
+
+    const int nk = (K + BK - 1) / BK;
+    load_tile(0, 0);
+    cp_async_commit();
+    for (int kt = 0; kt < nk; ++kt) {
+        if (kt + 1 < nk) load_tile(kt + 1, (kt + 1) & 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const T* as = As + (kt & 1) * BK * LA;
+        const T* bs = Bs + (kt & 1) * BK * LB;
+#pragma unroll 4
+        for (int k = 0; k < BK; ++k) {
+            T a[TM], b[TN];
+            load_frag<T, TM, WA>(a, as + k * LA, ty, TY);
+            load_frag<T, TN, WB>(b, bs + k * LB, tx, TX);
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = fmadd(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+
+    // out = alpha * acc + beta * C, C always read (kernels.py:227)
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int gm = m0 + tile_index<WA>(i, ty, TY);
+        if (gm >= M) continue;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            const int gn = n0 + tile_index<WB>(j, tx, TX);
+            if (gn < N) {
+                const T c = p.C[(i64)gm * p.ldc + gn];
+                p.out[(i64)gm * p.ldo + gn] = fmadd(p.alpha, acc[i][j], p.beta * c);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// indirect family: unpredicated multi-stage core on packed operands
+// ---------------------------------------------------------------------------
+template <typename T, int BM_, int BN_, int BK_, int TM, int TN, int UK, int STAGES>
+__global__ void __launch_bounds__(cta_threads_bound<T, BM_, BN_, TM, TN>())
+tiled_gemm_kernel(const TiledParams<T> p) {
+    constexpr bool FIXED = BM_ > 0 && BN_ > 0 && BK_ > 0;
+    constexpr int VL = FIXED ? VecW<T>::W : 1;  // elements per cp.async
+    constexpr int WA = FragW<T, TM>::W;
+    constexpr int WB = FragW<T, TN>::W;
+    const int BM = FIXED ? BM_ : p.bm;
+    const int BN = FIXED ? BN_ : p.bn;
+    const int BK = FIXED ? BK_ : p.bk;
+    const int TX = BN / TN, TY = BM / TM, NT = TX * TY;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* As = reinterpret_cast<T*>(smem_raw);  // [STAGES][BK][BM]
+    T* Bs = As + STAGES * BK * BM;            // [STAGES][BK][BN]
+
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+    const T* gA = p.At + m0;
+    const T* gB = p.Bp + n0;
+    auto load_tile = [&](int kt, int s) {
+        const int k0 = kt * BK;
+        T* as = As + s * BK * BM;
+        T* bs = Bs + s * BK * BN;
+        const int ca = BM / VL, cb = BN / VL;
+        for (int e = tid; e < BK * ca; e += NT) {
+            const int k = e / ca, c = e - k * ca;
+            cp_async<VL * sizeof(T)>(as + k * BM + c * VL, gA + (i64)(k0 + k) * p.lda + c * VL);
+        }
+        for (int e = tid; e < BK * cb; e += NT) {
+            const int k = e / cb, c = e - k * cb;
+            cp_async<VL * sizeof(T)>(bs + k * BN + c * VL, gB + (i64)(k0 + k) * p.ldb + c * VL);
+        }
+    };
+
+    const int nk = p.Kp / BK;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) load_tile(s, s);
+        cp_async_commit();
+    }
+    const int uk = FIXED ? UK : p.uk;
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + STAGES - 1;
+            if (nt < nk) load_tile(nt, nt % STAGES);
+            cp_async_commit();
+        }
+        const int s = kt % STAGES;
+        const T* as = As + s * BK * BM;
+        const T* bs = Bs + s * BK * BN;
+        if (FIXED) {
+#pragma unroll
+            for (int k = 0; k < BK; k += UK) {
+                T a[UK][TM], b[UK][TN];
+#pragma unroll
+                for (int u = 0; u < UK; ++u) {
+                    load_frag<T, TM, WA>(a[u], as + (k + u) * BM, ty, TY);
+                    load_frag<T, TN, WB>(b[u], bs + (k + u) * BN, tx, TX);
+                }
+#pragma unroll
+                for (int u = 0; u < UK; ++u)
+#pragma unroll
+                    for (int i = 0; i < TM; ++i)
+#pragma unroll
+                        for (int j = 0; j < TN; ++j) acc[i][j] = fmadd(a[u][i], b[u][j], acc[i][j]);
+            }
+        } else {
+            for (int k = 0; k < BK; k += uk) {
+                for (int u = 0; u < uk; ++u) {
+                    T a[TM], b[TN];
+                    load_frag<T, TM, WA>(a, as + (k + u) * BM, ty, TY);
+                    load_frag<T, TN, WB>(b, bs + (k + u) * BN, tx, TX);
+#pragma unroll
+                    for (int i = 0; i < TM; ++i)
+#pragma unroll
+                        for (int j = 0; j < TN; ++j) acc[i][j] = fmadd(a[i], b[j], acc[i][j]);
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+
+    // masked store epilogue (replaces outp + unpad copy, kernels.py:322-325)
+    const bool full = (m0 + BM <= p.M) && (n0 + BN <= p.N);
+    if (full && p.vec_out) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int gm = m0 + tile_index<WA>(i, ty, TY);
+#pragma unroll
+            for (int g = 0; g < TN / WB; ++g) {
+                const int gn = n0 + g * TX * WB + tx * WB;
+                Vec<T, WB> o;
+                if (p.use_c) {
+                    const Vec<T, WB> c = *reinterpret_cast<const Vec<T, WB>*>(p.C + (i64)gm * p.ldc + gn);
+#pragma unroll
+                    for (int e = 0; e < WB; ++e) o.v[e] = fmadd(p.alpha, acc[i][g * WB + e], p.beta * c.v[e]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < WB; ++e) o.v[e] = p.alpha * acc[i][g * WB + e];
+                }
+                *reinterpret_cast<Vec<T, WB>*>(p.out + (i64)gm * p.ldo + gn) = o;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int gm = m0 + tile_index<WA>(i, ty, TY);
+            if (gm >= p.M) continue;
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                const int gn = n0 + tile_index<WB>(j, tx, TX);
+                if (gn >= p.N) continue;
+                T v = p.alpha * acc[i][j];
+                if (p.use_c) v = fmadd(p.alpha, acc[i][j], p.beta * p.C[(i64)gm * p.ldc + gn]);
+                p.out[(i64)gm * p.ldo + gn] = v;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// helper passes and the parity oracle
+// ---------------------------------------------------------------------------
+
+// dst (dst_rows x dst_cols, ld_dst) = zero-padded L, where L (rows x cols) is
+// src (ld_src) itself or, with `transpose`, src stored cols x rows.
+// 32x32 tiles through shared memory keep both sides coalesced.
+template <typename T>
+__global__ void __launch_bounds__(256)
+pack_pad_kernel(T* __restrict__ dst, i64 ld_dst, int dst_rows, int dst_cols,
+                const T* __restrict__ src, i64 ld_src, int rows, int cols, int transpose) {
+    __shared__ T tile[32][33];
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    const int x = threadIdx.x, y = threadIdx.y;
+    if (transpose) {
+#pragma unroll
+        for (int yy = y; yy < 32; yy += 8) {
+            const int c = c0 + yy, r = r0 + x;  // src row c, col r (contiguous in r)
+            tile[yy][x] = (r < rows && c < cols) ? src[(i64)c * ld_src + r] : T(0);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int yy = y; yy < 32; yy += 8) {
+            const int r = r0 + yy, c = c0 + x;
+            if (r < dst_rows && c < dst_cols) dst[(i64)r * ld_dst + c] = tile[x][yy];
+        }
+    } else {
+#pragma unroll
+        for (int yy = y; yy < 32; yy += 8) {
+            const int r = r0 + yy, c = c0 + x;
+            if (r < dst_rows && c < dst_cols)
+                dst[(i64)r * ld_dst + c] = (r < rows && c < cols) ? src[(i64)r * ld_src + c] : T(0);
+        }
+    }
+}
+
+// Textbook (i, j, k) GEMM with float64 accumulation: every multiply and add
+// separately rounded (no FMA contraction), k ascending, then
+// alpha*acc + beta*C in float64 rounded once to T -- the same operation
+// sequence as _kernel_reference (kernels.py:184-195), hence bit-identical.
+template <typename T>
+__global__ void __launch_bounds__(256)
+reference_gemm_kernel(int M, int N, int K, double alpha, double beta, int ta, int tb,
+                      const T* __restrict__ A, i64 lda, const T* __restrict__ B, i64 ldb,
+                      const T* __restrict__ C, i64 ldc, T* __restrict__ out, i64 ldo) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (j >= N || i >= M) return;
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) {
+        const double a = (double)(ta ? A[(i64)k * lda + i] : A[(i64)i * lda + k]);
+        const double b = (double)(tb ? B[(i64)j * ldb + k] : B[(i64)k * ldb + j]);
+        acc = __dadd_rn(acc, __dmul_rn(a, b));
+    }
+    const double r = __dadd_rn(__dmul_rn(alpha, acc), __dmul_rn(beta, (double)C[(i64)i * ldc + j]));
+    out[(i64)i * ldo + j] = (T)r;
+}
+
+}  // namespace ag

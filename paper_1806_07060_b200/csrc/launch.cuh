@@ -1,0 +1,151 @@
+// launch.cuh -- host-side launchers for one kernel instantiation.
+//
+// A launcher runs the complete family path of one config on one stream:
+//   direct   : one predicated kernel on the caller's operands
+//   indirect : [pack op(A)^T] [pack op(B)] tiled core (masked epilogue);
+//              a pack is skipped when the operand already is a tile-multiple,
+//              16-byte aligned matrix in the layout the core streams
+//              (CLBlast-style "helpers only when needed").
+#pragma once
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "kernels.cuh"
+#include "registry.h"
+
+namespace ag {
+
+inline i64 round_up(i64 x, i64 s) { return (x + s - 1) / s * s; }
+
+// raise the per-kernel dynamic shared-memory limit once per needed size
+template <typename K>
+inline cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& granted) {
+    if (bytes <= 48 * 1024 || bytes <= granted.load(std::memory_order_relaxed)) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) {
+        size_t cur = granted.load();
+        while (bytes > cur && !granted.compare_exchange_weak(cur, bytes)) {
+        }
+    }
+    return e;
+}
+
+inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+inline int fail(const GemmCall& c, int code, const std::string& msg) {
+    if (c.err) *c.err = msg;
+    return code;
+}
+
+template <typename T>
+int launch_pack(T* dst, i64 ld_dst, i64 dst_rows, i64 dst_cols, const T* src, i64 ld_src,
+                i64 rows, i64 cols, int transpose, cudaStream_t stream) {
+    dim3 grid((unsigned)((dst_cols + 31) / 32), (unsigned)((dst_rows + 31) / 32));
+    if (grid.y > 65535u) return AG_ERR_SHAPE;
+    pack_pad_kernel<T><<<grid, dim3(32, 8), 0, stream>>>(dst, ld_dst, (int)dst_rows, (int)dst_cols, src, ld_src,
+                                                         (int)rows, (int)cols, transpose);
+    return cudaGetLastError() == cudaSuccess ? AG_OK : AG_ERR_CUDA;
+}
+
+template <typename T, int BM, int BN, int BK, int TM, int TN>
+int launch_direct(const GemmCall& c) {
+    const int bm = BM ? BM : c.bm, bn = BN ? BN : c.bn, bk = BK ? BK : c.bk;
+    const int threads = (bm / TM) * (bn / TN);
+    if (threads > cta_threads_bound<T, BM, BN, TM, TN>())
+        return fail(c, AG_ERR_CONFIG, "config needs more threads per CTA than its kernel supports");
+    const size_t smem = direct_smem_bytes<T>(bm, bn, bk);
+    if (smem > 227 * 1024) return fail(c, AG_ERR_CONFIG, "config exceeds 227 KB shared memory per CTA");
+    auto kernel = direct_gemm_kernel<T, BM, BN, BK, TM, TN>;
+    static std::atomic<size_t> granted{0};
+    if (ensure_smem(kernel, smem, granted) != cudaSuccess) return fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
+    const i64 gy = (c.M + bm - 1) / bm, gx = (c.N + bn - 1) / bn;
+    if (gy > 65535 || gx > 0x7fffffff) return fail(c, AG_ERR_SHAPE, "problem too large for the direct grid");
+    DirectParams<T> p;
+    p.M = (int)c.M; p.N = (int)c.N; p.K = (int)c.K;
+    p.alpha = (T)c.alpha; p.beta = (T)c.beta;
+    p.ta = c.ta; p.tb = c.tb;
+    p.A = static_cast<const T*>(c.A); p.lda = c.lda;
+    p.B = static_cast<const T*>(c.B); p.ldb = c.ldb;
+    p.C = static_cast<const T*>(c.C); p.ldc = c.ldc;
+    p.out = static_cast<T*>(c.out); p.ldo = c.ldo;
+    p.bm = bm; p.bn = bn; p.bk = bk;
+    kernel<<<dim3((unsigned)gx, (unsigned)gy), threads, smem, c.stream>>>(p);
+    return cudaGetLastError() == cudaSuccess ? AG_OK : fail(c, AG_ERR_CUDA, "direct kernel launch failed");
+}
+
+template <typename T>
+size_t indirect_workspace_bytes(i64 M, i64 N, i64 K, int bm, int bn, int bk) {
+    const i64 Mp = round_up(M, bm), Np = round_up(N, bn), Kp = round_up(K, bk);
+    return (size_t)round_up(Kp * Mp * (i64)sizeof(T), 256) + (size_t)round_up(Kp * Np * (i64)sizeof(T), 256);
+}
+
+template <typename T, int BM, int BN, int BK, int TM, int TN, int UK>
+int launch_indirect(const GemmCall& c) {
+    constexpr bool FIXED = BM > 0 && BN > 0 && BK > 0;
+    constexpr int STAGES = tiled_stages<T>(BM, BN, BK);
+    constexpr int VL = FIXED ? VecW<T>::W : 1;
+    constexpr int WB = FragW<T, TN>::W;
+    const int bm = FIXED ? BM : c.bm, bn = FIXED ? BN : c.bn, bk = FIXED ? BK : c.bk;
+    const int uk = FIXED ? UK : c.uk;
+    const int threads = (bm / TM) * (bn / TN);
+    if (threads > cta_threads_bound<T, BM, BN, TM, TN>())
+        return fail(c, AG_ERR_CONFIG, "config needs more threads per CTA than its kernel supports");
+    if (bk % uk) return fail(c, AG_ERR_CONFIG, "block_k must be a multiple of unroll_k");
+    const size_t smem = tiled_smem_bytes<T>(bm, bn, bk, STAGES);
+    if (smem > 227 * 1024) return fail(c, AG_ERR_CONFIG, "config exceeds 227 KB shared memory per CTA");
+    auto kernel = tiled_gemm_kernel<T, BM, BN, BK, TM, TN, UK, STAGES>;
+    static std::atomic<size_t> granted{0};
+    if (ensure_smem(kernel, smem, granted) != cudaSuccess) return fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
+
+    const i64 M = c.M, N = c.N, K = c.K;
+    const i64 Mp = round_up(M, bm), Np = round_up(N, bn), Kp = round_up(K, bk);
+    if (Mp / bm > 65535) return fail(c, AG_ERR_SHAPE, "problem too large for the indirect grid");
+    if (Mp > 0x7fffffff || Np > 0x7fffffff || Kp > 0x7fffffff) return fail(c, AG_ERR_SHAPE, "dimension too large");
+    const size_t need = indirect_workspace_bytes<T>(M, N, K, bm, bn, bk);
+    if (c.ws_bytes < need || (need && c.ws == nullptr))
+        return fail(c, AG_ERR_SHAPE, "workspace too small for the indirect pack buffers");
+    const size_t va = VL * sizeof(T);
+
+    // op(A)^T, K-major (Kp x Mp): A itself when transA and already padded
+    const T* At;
+    i64 lda_t;
+    T* wsA = static_cast<T*>(c.ws);
+    T* wsB = reinterpret_cast<T*>(static_cast<char*>(c.ws) + round_up(Kp * Mp * (i64)sizeof(T), 256));
+    if (c.ta && M == Mp && K == Kp && c.lda % VL == 0 && aligned(c.A, va)) {
+        At = static_cast<const T*>(c.A);
+        lda_t = c.lda;
+    } else {
+        int r = launch_pack<T>(wsA, Mp, Kp, Mp, static_cast<const T*>(c.A), c.lda, K, M, c.ta ? 0 : 1, c.stream);
+        if (r) return fail(c, r, "pack of op(A) failed");
+        At = wsA;
+        lda_t = Mp;
+    }
+    const T* Bp;
+    i64 ldb_p;
+    if (!c.tb && N == Np && K == Kp && c.ldb % VL == 0 && aligned(c.B, va)) {
+        Bp = static_cast<const T*>(c.B);
+        ldb_p = c.ldb;
+    } else {
+        int r = launch_pack<T>(wsB, Np, Kp, Np, static_cast<const T*>(c.B), c.ldb, K, N, c.tb ? 1 : 0, c.stream);
+        if (r) return fail(c, r, "pack of op(B) failed");
+        Bp = wsB;
+        ldb_p = Np;
+    }
+
+    TiledParams<T> p;
+    p.Mp = (int)Mp; p.Np = (int)Np; p.Kp = (int)Kp; p.M = (int)M; p.N = (int)N;
+    p.alpha = (T)c.alpha; p.beta = (T)c.beta;
+    p.use_c = c.beta != 0.0;
+    const size_t wb = WB * sizeof(T);
+    p.vec_out = (c.ldo % WB == 0) && aligned(c.out, wb) && (!p.use_c || ((c.ldc % WB == 0) && aligned(c.C, wb)));
+    p.At = At; p.lda = lda_t;
+    p.Bp = Bp; p.ldb = ldb_p;
+    p.C = static_cast<const T*>(c.C); p.ldc = c.ldc;
+    p.out = static_cast<T*>(c.out); p.ldo = c.ldo;
+    p.bm = bm; p.bn = bn; p.bk = bk; p.uk = uk;
+    kernel<<<dim3((unsigned)(Np / bn), (unsigned)(Mp / bm)), threads, smem, c.stream>>>(p);
+    return cudaGetLastError() == cudaSuccess ? AG_OK : fail(c, AG_ERR_CUDA, "indirect kernel launch failed");
+}
+
+}  // namespace ag

@@ -1,0 +1,414 @@
+"""GEMM problem/config types, the legal search space, and the device GEMM path.
+
+Drop-in for `adaptgemm.kernels` (/root/reference/pkg/src/adaptgemm/
+kernels.py).  Types, legality rules and enumeration order are the
+reference's; execution is not: `gemm_execute` runs the family path as
+sm_100a CUDA kernels from libadaptgemm_b200.so (csrc/kernels.cuh):
+
+* direct   -- one predicated kernel on the caller's unpadded operands,
+              transposes and ragged edges handled in-kernel (kernels.py:198-227);
+* indirect -- pack/transpose-pad helper kernels into tile-multiple buffers,
+              then the branch-free tiled core (kernels.py:230-260, 304-325).
+
+Operands may be numpy arrays (staged to the GPU, result copied back -- the
+reference's calling convention) or CUDA torch tensors (used in place).
+`seconds` is the device time of the family path, measured with CUDA events
+on the launching stream (helpers included, allocation and host<->device
+copies excluded).  There is no CPU fallback: without a GPU or without the
+built library these functions raise.
+"""
+
+import ctypes
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _device, _native, spaces
+
+
+class ShapeError(ValueError):
+    """Operand dimensions are inconsistent with the problem shape."""
+
+
+class ConfigError(ValueError):
+    """Kernel configuration is invalid or illegal for the device caps."""
+
+
+class KernelFamily(str, Enum):
+    DIRECT = "direct"
+    INDIRECT = "indirect"
+
+
+_FAMILY_CODE = {KernelFamily.DIRECT: _native.AG_FAMILY_DIRECT,
+                KernelFamily.INDIRECT: _native.AG_FAMILY_INDIRECT}
+
+
+@dataclass(frozen=True)
+class ProblemShape:
+    """One GEMM problem: C = alpha * op(A) @ op(B) + beta * C (kernels.py:37-61).
+
+    op(A) is M x K and op(B) is K x N; transA/transB describe the stored
+    layout of A and B relative to that.
+    """
+
+    M: int
+    N: int
+    K: int
+    alpha: float = 1.0
+    beta: float = 0.0
+    transA: bool = False
+    transB: bool = False
+
+    def __post_init__(self):
+        for name in ("M", "N", "K"):
+            v = getattr(self, name)
+            if isinstance(v, bool) or not isinstance(v, int) or v < 1:
+                raise ShapeError(f"{name} must be a positive integer, got {v!r}")
+
+    @property
+    def mnk(self) -> tuple[int, int, int]:
+        return (self.M, self.N, self.K)
+
+
+@dataclass(frozen=True)
+class DeviceCaps:
+    """Resource limits deciding which configs are legal (kernels.py:64-82).
+
+    The first four fields and their defaults are the reference's.  Two
+    B200 fields follow: `max_threads` (threads per CTA) and `profile`, which
+    selects the enumerated domains -- "reference" (144 direct / 432
+    indirect) or "b200" (the reference domains plus large CTA tiles, see
+    spaces.py).  `DeviceCaps.b200()` returns the B200 tuning profile.
+    """
+
+    tile_memory_cap: int = 32768
+    register_tile_cap_direct: int = 8
+    register_tile_cap_indirect: int = 32
+    element_size: int = 4
+    max_threads: int = 1024
+    profile: str = spaces.PROFILE_REFERENCE
+
+    def __post_init__(self):
+        for name in ("tile_memory_cap", "register_tile_cap_direct",
+                     "register_tile_cap_indirect", "element_size", "max_threads"):
+            if getattr(self, name) < 1:
+                raise ConfigError(f"{name} must be positive")
+        if self.profile not in (spaces.PROFILE_REFERENCE, spaces.PROFILE_B200):
+            raise ConfigError(f"unknown caps profile {self.profile!r}")
+
+    @classmethod
+    def b200(cls, **overrides) -> "DeviceCaps":
+        kw = dict(spaces.B200_CAPS)
+        kw["profile"] = spaces.PROFILE_B200
+        kw.update(overrides)
+        return cls(**kw)
+
+    def register_tile_cap(self, family: KernelFamily) -> int:
+        if family is KernelFamily.DIRECT:
+            return self.register_tile_cap_direct
+        return self.register_tile_cap_indirect
+
+    def as_dict(self) -> dict:
+        return dict(tile_memory_cap=self.tile_memory_cap,
+                    register_tile_cap_direct=self.register_tile_cap_direct,
+                    register_tile_cap_indirect=self.register_tile_cap_indirect,
+                    element_size=self.element_size, max_threads=self.max_threads)
+
+    def native(self) -> _native.AgCaps:
+        return _native.AgCaps(self.tile_memory_cap, self.register_tile_cap_direct,
+                              self.register_tile_cap_indirect, self.element_size, self.max_threads)
+
+
+@dataclass(frozen=True, order=True)
+class KernelConfig:
+    """Family plus tuning parameters (kernels.py:85-119).
+
+    block_m/block_n: CTA tile; block_k: K depth of one shared-memory stage;
+    tile_m/tile_n: per-thread register tile; unroll_k: K steps whose register
+    fragments are loaded ahead of the FMAs (indirect only; 1 for direct).
+    Field order defines the canonical total order.
+    """
+
+    family: KernelFamily
+    block_m: int
+    block_n: int
+    block_k: int
+    tile_m: int
+    tile_n: int
+    unroll_k: int = 1
+
+    def canonical(self) -> str:
+        """Stable textual identity; equal strings mean the same class."""
+        return (f"{self.family.value}:{self.block_m}-{self.block_n}-{self.block_k}"
+                f"-{self.tile_m}-{self.tile_n}-{self.unroll_k}")
+
+    def param_tuple(self) -> tuple[int, int, int, int, int, int]:
+        return (self.block_m, self.block_n, self.block_k,
+                self.tile_m, self.tile_n, self.unroll_k)
+
+    @classmethod
+    def from_canonical(cls, text: str) -> "KernelConfig":
+        try:
+            fam, params = text.split(":")
+            bm, bn, bk, tm, tn, uk = (int(p) for p in params.split("-"))
+            family = KernelFamily(fam)
+        except ValueError as exc:
+            raise ConfigError(f"bad canonical config {text!r}") from exc
+        return cls(family, bm, bn, bk, tm, tn, uk)
+
+    def native(self) -> _native.AgConfig:
+        return _native.AgConfig(_FAMILY_CODE[self.family], *self.param_tuple())
+
+    @classmethod
+    def from_native(cls, c: _native.AgConfig) -> "KernelConfig":
+        fam = KernelFamily.DIRECT if c.family == _native.AG_FAMILY_DIRECT else KernelFamily.INDIRECT
+        return cls(fam, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk)
+
+
+# Parameter domains for exhaustive enumeration, in canonical order (kernels.py:123-138)
+DIRECT_DOMAINS = spaces.DIRECT_DOMAINS
+INDIRECT_DOMAINS = spaces.INDIRECT_DOMAINS
+
+
+def domains_for(family: KernelFamily) -> dict[str, tuple[int, ...]]:
+    return DIRECT_DOMAINS if family is KernelFamily.DIRECT else INDIRECT_DOMAINS
+
+
+def _caps_dict(caps: DeviceCaps) -> dict:
+    return caps.as_dict()
+
+
+def is_legal(config: KernelConfig, caps: DeviceCaps) -> bool:
+    """Every configuration invariant under the given caps (kernels.py:145-158)."""
+    return spaces.is_legal_tuple(config.family.value, *config.param_tuple(), _caps_dict(caps))
+
+
+def enumerate_search_space(family: KernelFamily, caps: DeviceCaps = DeviceCaps()) -> list[KernelConfig]:
+    """All legal configs of one family in deterministic canonical order."""
+    fam = KernelFamily(family)
+    return [KernelConfig(fam, *t[1:])
+            for t in spaces.enumerate_tuples(fam.value, _caps_dict(caps), caps.profile)]
+
+
+def full_search_space(caps: DeviceCaps = DeviceCaps()) -> list[KernelConfig]:
+    """Both families concatenated: direct block first, then indirect."""
+    return (enumerate_search_space(KernelFamily.DIRECT, caps)
+            + enumerate_search_space(KernelFamily.INDIRECT, caps))
+
+
+# ---------------------------------------------------------------------------
+# operands
+
+
+def _round_up(x: int, step: int) -> int:
+    return -(-x // step) * step
+
+
+def _dims(x) -> tuple:
+    return tuple(int(d) for d in x.shape)
+
+
+def _check_operands(shape: ProblemShape, A, B, C):
+    """kernels.py:271-283, for numpy arrays and CUDA torch tensors alike."""
+    a_dims = (shape.K, shape.M) if shape.transA else (shape.M, shape.K)
+    b_dims = (shape.N, shape.K) if shape.transB else (shape.K, shape.N)
+    if A.ndim != 2 or _dims(A) != a_dims:
+        raise ShapeError(f"A has shape {_dims(A)}, expected {a_dims}")
+    if B.ndim != 2 or _dims(B) != b_dims:
+        raise ShapeError(f"B has shape {_dims(B)}, expected {b_dims}")
+    if C.ndim != 2 or _dims(C) != (shape.M, shape.N):
+        raise ShapeError(f"C has shape {_dims(C)}, expected {(shape.M, shape.N)}")
+    if not (A.dtype == B.dtype == C.dtype):
+        raise ShapeError(f"mixed dtypes: {A.dtype}, {B.dtype}, {C.dtype}")
+    if _device.dtype_code(A.dtype) < 0:
+        raise ShapeError(f"unsupported dtype {A.dtype}, want float32 or float64")
+
+
+class _Operands:
+    """Device views of (A, B, C, out) for one call, host or device side."""
+
+    def __init__(self, shape: ProblemShape, A, B, C, out):
+        self.host = not any(_device.is_device_tensor(x) for x in (A, B, C))
+        t = _device.require_cuda()
+        self.code = _device.dtype_code(A.dtype)
+        if self.host:
+            if out is not None and (_dims(out) != (shape.M, shape.N) or out.dtype != A.dtype):
+                raise ShapeError("out buffer has wrong shape or dtype")
+            self.device = _device.default_device()
+            self.A = _device.to_device(A, self.device)
+            self.B = _device.to_device(B, self.device)
+            self.C = _device.to_device(C, self.device)
+            self.out_host = out
+            self.out = t.empty((shape.M, shape.N), dtype=self.A.dtype, device=self.device)
+        else:
+            for name, x in (("A", A), ("B", B), ("C", C)):
+                if not _device.is_device_tensor(x) or not x.is_cuda:
+                    raise ShapeError(f"{name} must be a CUDA tensor when any operand is one")
+            self.device = A.device
+            if B.device != self.device or C.device != self.device:
+                raise ShapeError("operands live on different devices")
+            self.A = _device.row_major(A)
+            self.B = _device.row_major(B)
+            self.C = _device.row_major(C)
+            if out is None:
+                out = t.empty((shape.M, shape.N), dtype=A.dtype, device=self.device)
+            elif (not _device.is_device_tensor(out) or _dims(out) != (shape.M, shape.N)
+                  or out.dtype != A.dtype or out.device != self.device):
+                raise ShapeError("out buffer has wrong shape, dtype or device")
+            self.out_host = None
+            self.out_user = out
+            self.out = out if (out.stride(1) == 1 and out.stride(0) >= shape.N) else \
+                t.empty((shape.M, shape.N), dtype=A.dtype, device=self.device)
+
+    def args(self):
+        ld = _device.leading_dim
+        return (ctypes.c_void_p(self.A.data_ptr()), ld(self.A),
+                ctypes.c_void_p(self.B.data_ptr()), ld(self.B),
+                ctypes.c_void_p(self.C.data_ptr()), ld(self.C),
+                ctypes.c_void_p(self.out.data_ptr()), ld(self.out))
+
+    def result(self):
+        if self.host:
+            res = self.out.cpu().numpy()
+            if self.out_host is not None:
+                self.out_host[...] = res
+                return self.out_host
+            return res
+        if self.out is not self.out_user:
+            self.out_user.copy_(self.out)
+        return self.out_user
+
+
+def _raise_for(code: int, config: "KernelConfig | None" = None):
+    msg = _native.last_error()
+    if code == _native.AG_ERR_CONFIG:
+        raise ConfigError(msg or f"illegal config {config.canonical() if config else ''}")
+    if code == _native.AG_ERR_SHAPE:
+        raise ShapeError(msg)
+    raise RuntimeError(f"CUDA failure in adaptgemm-b200: {msg}")
+
+
+def native_shape(shape: ProblemShape) -> _native.AgShape:
+    return _native.AgShape(shape.M, shape.N, shape.K, float(shape.alpha), float(shape.beta),
+                           int(bool(shape.transA)), int(bool(shape.transB)))
+
+
+def workspace_bytes(shape: ProblemShape, config: KernelConfig, dtype=np.float32) -> int:
+    """Device bytes the indirect pack buffers need (0 for direct)."""
+    code = _device.dtype_code(dtype)
+    return int(_native.lib().ag_workspace_bytes(ctypes.byref(native_shape(shape)),
+                                                 ctypes.byref(config.native()), max(code, 0)))
+
+
+# ---------------------------------------------------------------------------
+# public entry points
+
+
+def gemm_reference(shape: ProblemShape, A, B, C, out=None):
+    """Textbook (i, j, k) GEMM with float64 accumulation; the correctness oracle.
+
+    Runs `reference_gemm_kernel` on the GPU: the operation sequence of
+    _kernel_reference (kernels.py:184-195) -- separately rounded float64
+    multiply and add in k order, one rounding to the element type -- so the
+    result is bit-identical to the reference's.
+    """
+    _check_operands(shape, A, B, C)
+    ops = _Operands(shape, A, B, C, out)
+    lib = _native.lib()
+    a, lda, b, ldb, c, ldc, o, ldo = ops.args()
+    rc = lib.ag_gemm_reference(ctypes.byref(native_shape(shape)), ops.code, a, lda, b, ldb, c, ldc,
+                               o, ldo, ctypes.c_void_p(_device.current_stream_handle(ops.device)))
+    if rc:
+        _raise_for(rc)
+    return ops.result()
+
+
+def pack_padded(X, rows: int, cols: int, transpose: bool, pad_rows: int, pad_cols: int):
+    """Indirect-family helper pass: zero-padded copy of op(X) (kernels.py:304-309).
+
+    Runs the device pack kernel; numpy in -> numpy out, CUDA tensor in ->
+    CUDA tensor out.
+    """
+    t = _device.require_cuda()
+    host = not _device.is_device_tensor(X)
+    code = _device.dtype_code(X.dtype)
+    if code < 0:
+        raise ShapeError(f"unsupported dtype {X.dtype}")
+    dev = _device.default_device() if host else X.device
+    src = _device.to_device(X, dev) if host else _device.row_major(X)
+    want = (cols, rows) if transpose else (rows, cols)
+    if _dims(src) != want:
+        raise ShapeError(f"X has shape {_dims(src)}, expected {want}")
+    dst = t.empty((pad_rows, pad_cols), dtype=src.dtype, device=dev)
+    rc = _native.lib().ag_pack_padded(code, ctypes.c_void_p(src.data_ptr()), _device.leading_dim(src),
+                                      rows, cols, int(bool(transpose)), ctypes.c_void_p(dst.data_ptr()),
+                                      pad_rows, pad_cols, ctypes.c_void_p(_device.current_stream_handle(dev)))
+    if rc:
+        _raise_for(rc)
+    return dst.cpu().numpy() if host else dst
+
+
+def _launch(shape: ProblemShape, config: KernelConfig, caps: DeviceCaps, ops: _Operands,
+            timed: bool) -> float:
+    t = _device.torch()
+    lib = _native.lib()
+    nshape, ncfg, ncaps = native_shape(shape), config.native(), caps.native()
+    ws_n = int(lib.ag_workspace_bytes(ctypes.byref(nshape), ctypes.byref(ncfg), ops.code))
+    ws = _device.workspace(ws_n, ops.device) if ws_n else None
+    ws_ptr = ctypes.c_void_p(ws.data_ptr() if ws is not None else 0)
+    stream = t.cuda.current_stream(ops.device)
+    a, lda, b, ldb, c, ldc, o, ldo = ops.args()
+    if timed:
+        e0 = t.cuda.Event(enable_timing=True)
+        e1 = t.cuda.Event(enable_timing=True)
+        e0.record(stream)
+    rc = lib.ag_gemm(ctypes.byref(nshape), ctypes.byref(ncfg), ctypes.byref(ncaps), ops.code,
+                     a, lda, b, ldb, c, ldc, o, ldo, ws_ptr, ws_n, ctypes.c_void_p(stream.cuda_stream))
+    if rc:
+        _raise_for(rc, config)
+    if not timed:
+        return 0.0
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) * 1e-3
+
+
+def gemm_execute(shape: ProblemShape, config: KernelConfig, A, B, C,
+                 caps: DeviceCaps = DeviceCaps(), out=None):
+    """Run one config's family path end to end on the GPU (kernels.py:328-349).
+
+    Legality is checked before the operands (ConfigError, then ShapeError).
+    Returns (result, seconds); seconds is the CUDA-event device time of the
+    whole family path (indirect: pack helpers + tiled core), floored at 1e-9.
+    """
+    if not is_legal(config, caps):
+        raise ConfigError(f"illegal config {config.canonical()} for caps {caps}")
+    _check_operands(shape, A, B, C)
+    ops = _Operands(shape, A, B, C, out)
+    elapsed = _launch(shape, config, caps, ops, timed=True)
+    return ops.result(), max(elapsed, 1e-9)
+
+
+def warm_kernels(dtype=np.float32) -> None:
+    """Initialise the CUDA context and load the kernel module (kernels.py:352-361)."""
+    shape = ProblemShape(4, 4, 4, alpha=1.0, beta=1.0)
+    A = np.ones((4, 4), dtype)
+    B = np.ones((4, 4), dtype)
+    C = np.ones((4, 4), dtype)
+    gemm_reference(shape, A, B, C)
+    gemm_execute(shape, KernelConfig(KernelFamily.DIRECT, 8, 8, 8, 2, 2, 1), A, B, C)
+    for uk in (1, 2):
+        gemm_execute(shape, KernelConfig(KernelFamily.INDIRECT, 16, 16, 8, 2, 2, uk), A, B, C)
+
+
+def ffma_peak_tflops() -> float:
+    """Measured FP32 FFMA throughput of this GPU (CUDA-core roofline)."""
+    t = _device.require_cuda()
+    dev = _device.default_device()
+    val = ctypes.c_double(0.0)
+    rc = _native.lib().ag_ffma_peak(ctypes.c_void_p(t.cuda.current_stream(dev).cuda_stream),
+                                    ctypes.byref(val))
+    if rc:
+        _raise_for(rc)
+    return val.value

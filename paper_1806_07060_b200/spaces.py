@@ -1,0 +1,127 @@
+"""Tuning-parameter domains and legality rules (dependency-free).
+
+Restates the reference's parameter space (/root/reference/pkg/src/adaptgemm/
+kernels.py:122-177) and adds the explicit B200 profile.  The build script
+imports this module to decide which sm_100a kernel instantiations to
+compile, so it must stay importable without numpy/torch.
+
+Config tuples are ``(family, bm, bn, bk, tm, tn, uk)`` with family
+``"direct"`` or ``"indirect"``.
+"""
+
+import itertools
+
+# kernels.py:123-138 -- the reference domains, canonical order
+DIRECT_DOMAINS = {
+    "block_m": (8, 16, 32),
+    "block_n": (8, 16, 32),
+    "block_k": (8, 16),
+    "tile_m": (1, 2, 4),
+    "tile_n": (1, 2, 4),
+    "unroll_k": (1,),
+}
+INDIRECT_DOMAINS = {
+    "block_m": (16, 32, 64),
+    "block_n": (16, 32, 64),
+    "block_k": (8, 16, 32),
+    "tile_m": (2, 4, 8),
+    "tile_n": (2, 4, 8),
+    "unroll_k": (1, 2),
+}
+
+# B200 profile: the reference space plus large CTA tiles that only pay off
+# on a 148-SM part with 227 KB of shared memory per CTA.  Enumerated after
+# the reference configs so that reference-profile class ids keep their
+# meaning.  Kept small on purpose: every entry is a compiled instantiation.
+B200_INDIRECT_EXTRA_DOMAINS = {
+    "block_m": (64, 128, 256),
+    "block_n": (64, 128, 256),
+    "block_k": (8, 16, 32),
+    "tile_m": (4, 8),
+    "tile_n": (4, 8),
+    "unroll_k": (1, 2),
+}
+
+PROFILE_REFERENCE = "reference"
+PROFILE_B200 = "b200"
+
+# DeviceCaps defaults (kernels.py:64-71) and the B200 profile caps
+REFERENCE_CAPS = dict(tile_memory_cap=32768, register_tile_cap_direct=8,
+                      register_tile_cap_indirect=32, element_size=4, max_threads=1024)
+B200_CAPS = dict(tile_memory_cap=65536, register_tile_cap_direct=8,
+                 register_tile_cap_indirect=64, element_size=4, max_threads=1024)
+
+REGISTER_FILE = 65536  # 32-bit registers per SM (and per CTA) on sm_100
+
+_FIELDS = ("block_m", "block_n", "block_k", "tile_m", "tile_n", "unroll_k")
+
+
+def is_legal_tuple(family, bm, bn, bk, tm, tn, uk, caps) -> bool:
+    """kernels.is_legal (kernels.py:145-158) + two sm_100 launch limits.
+
+    The CTA thread limit (bm/tm)*(bn/tn) <= max_threads and the register
+    file limit threads * (tm*tn + tm + tn + 24) <= 65536 (accumulators,
+    fragments and ~24 addressing registers per thread) never bind on the
+    reference domains under the reference caps (their maxima are 1024
+    threads and 32768 registers), so the 144/432 legal counts are unchanged.
+    """
+    if min(bm, bn, bk, tm, tn, uk) < 1:
+        return False
+    if family == "direct" and uk != 1:
+        return False
+    if bm % tm or bn % tn or bk % uk:
+        return False
+    cap = caps["register_tile_cap_direct"] if family == "direct" else caps["register_tile_cap_indirect"]
+    if tm * tn > cap:
+        return False
+    if (bm + bn) * bk * caps["element_size"] > caps["tile_memory_cap"]:
+        return False
+    threads = (bm // tm) * (bn // tn)
+    if threads > caps.get("max_threads", 1024):
+        return False
+    if threads * (tm * tn + tm + tn + 24) > REGISTER_FILE:
+        return False
+    return True
+
+
+def _product(family, domains):
+    for vals in itertools.product(*(domains[f] for f in _FIELDS)):
+        yield (family,) + vals
+
+
+def enumerate_tuples(family, caps, profile=PROFILE_REFERENCE):
+    """Legal configs of one family in deterministic canonical order."""
+    base = DIRECT_DOMAINS if family == "direct" else INDIRECT_DOMAINS
+    out = [t for t in _product(family, base) if is_legal_tuple(*t, caps)]
+    if profile == PROFILE_B200 and family == "indirect":
+        seen = set(out)
+        for t in _product(family, B200_INDIRECT_EXTRA_DOMAINS):
+            bm, bn = t[1], t[2]
+            if max(bm, bn) < 128 or t in seen:
+                continue
+            # big tiles only with >= 64 threads: a 148-SM part needs warps
+            if (bm // t[4]) * (bn // t[5]) < 64:
+                continue
+            if is_legal_tuple(*t, caps):
+                out.append(t)
+                seen.add(t)
+    return out
+
+
+def compiled_tuples():
+    """Every (family, bm, bn, bk, tm, tn, uk) with a fully templated fp32
+    kernel: both profiles' enumerations under their own caps."""
+    out = []
+    seen = set()
+    for profile, caps in ((PROFILE_REFERENCE, REFERENCE_CAPS), (PROFILE_B200, B200_CAPS)):
+        for fam in ("direct", "indirect"):
+            for t in enumerate_tuples(fam, caps, profile):
+                if t not in seen:
+                    seen.add(t)
+                    out.append(t)
+    return out
+
+
+# register-tile shapes with a run-time-tile-size kernel (any bm/bn/bk):
+# float64 runs these, as do legal float32 configs outside the domains
+RUNTIME_TILES = (1, 2, 4, 8)
