@@ -1,0 +1,115 @@
+"""Dispatch (compiled selector + GPU launch) and the full CLI pipeline on the GPU."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import rand_operands
+from paper_1806_07060_b200 import codegen, evaluation
+from paper_1806_07060_b200 import model as M
+from paper_1806_07060_b200.dataset import dataset_from_tables, gen_po2
+from paper_1806_07060_b200.kernels import DeviceCaps, KernelConfig, KernelFamily, ProblemShape, gemm_execute
+
+pytestmark = pytest.mark.gpu
+
+FIXTURE = [((64, 1, 1), 0), ((128, 1, 1), 0), ((256, 1, 1), 1), ((512, 1, 1), 1)]
+SIDE = {0: KernelConfig(KernelFamily.DIRECT, 16, 16, 8, 2, 2, 1),
+        1: KernelConfig(KernelFamily.INDIRECT, 32, 32, 16, 4, 4, 2)}
+
+
+@pytest.fixture(scope="module")
+def fixture_tree():
+    return M.train(FIXTURE, M.TrainConfig(max_height=1))
+
+
+def test_dispatch_bit_identical_to_direct_call(fixture_tree):
+    s = ProblemShape(33, 20, 15, alpha=1.25, beta=0.5)
+    A, B, C = rand_operands(s, seed=31)
+    res = codegen.dispatch_and_run(fixture_tree, s, A, B, C, classes=SIDE)
+    direct, _ = gemm_execute(s, res.selected, A, B, C)
+    np.testing.assert_array_equal(res.output, direct)
+    assert res.selected == SIDE[0] and not res.used_fallback and res.exec_seconds > 0
+
+
+def test_dispatch_sources_and_selector(fixture_tree):
+    s = ProblemShape(256, 8, 8)
+    A, B, C = rand_operands(s, seed=37)
+    for model in (codegen.emit_dispatcher(fixture_tree, SIDE, "python"),
+                  codegen.CompiledSelector(fixture_tree, SIDE)):
+        res = codegen.dispatch_and_run(model, s, A, B, C)
+        assert res.selected == SIDE[M.predict(fixture_tree, s.mnk)]
+
+
+def test_dispatch_fallback(fixture_tree):
+    caps = DeviceCaps(register_tile_cap_indirect=2)
+    s = ProblemShape(256, 8, 8)
+    A, B, C = rand_operands(s, seed=41)
+    res = codegen.dispatch_and_run(fixture_tree, s, A, B, C, caps=caps, classes=SIDE)
+    assert res.used_fallback and res.selected.family is KernelFamily.DIRECT
+    ref, _ = gemm_execute(s, res.selected, A, B, C, caps)
+    np.testing.assert_array_equal(res.output, ref)
+    sel = codegen.CompiledSelector(fixture_tree, SIDE)
+    out, picked, fb = codegen.dispatch_native(sel, s, A, B, C, caps)
+    assert fb and picked == codegen.FALLBACK_CONFIG
+    np.testing.assert_array_equal(out, ref)
+
+
+def test_dispatch_native_device_tensors(fixture_tree):
+    import torch
+    sel = codegen.CompiledSelector(fixture_tree, SIDE)
+    s = ProblemShape(512, 300, 200, alpha=1.0, beta=0.5)
+    A, B, C = rand_operands(s, seed=2)
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+    out, picked, fb = codegen.dispatch_native(sel, s, dA, dB, dC)
+    assert picked == SIDE[1] and not fb
+    ref, _ = gemm_execute(s, picked, A, B, C)
+    np.testing.assert_array_equal(out.cpu().numpy(), ref)
+
+
+def test_overhead_below_one_percent(fake_table_factory):
+    tables = [fake_table_factory(s) for s in gen_po2(64, 512)]
+    ds = dataset_from_tables(tables, "po2")
+    tree = M.train(ds.features_and_labels())
+    samples = evaluation.overhead_bench(tree, [ProblemShape(1024, 1024, 1024)], 20, ds.class_index)
+    s = samples[0]
+    assert s.dispatch_ns < 1000 and s.overhead_fraction < 0.01
+
+
+def _config(tmp, out, **over):
+    shapes = tmp / "shapes.txt"
+    shapes.write_text("8 8 8\n16 16 16\n24 24 24\n32 32 32\n")
+    doc = {"out_dir": str(out), "timing": {"warmup": 0, "repeats": 1},
+           "dataset": {"strategy": "workload", "path": str(shapes)},
+           "split": {"fraction": 0.5, "seed": 7}, "grid": {"heights": [1, "max"], "min_leaf": [1]},
+           "baseline": {"threshold": 16, "direct_anchor": [8, 8, 8], "indirect_anchor": [32, 32, 32]}}
+    doc.update(over)
+    p = tmp / "config.json"
+    p.write_text(json.dumps(doc))
+    return p
+
+
+def test_cli_pipeline_on_gpu(tmp_path, capsys):
+    from paper_1806_07060_b200.cli import main
+    out = tmp_path / "run"
+    cfg = _config(tmp_path, out)
+    for stage in ("tune", "dataset", "train", "eval", "codegen", "bench"):
+        assert main([stage, "--config", str(cfg)]) == 0, stage
+    for name in ("dataset.csv", "split.json", "scores.csv", "best_model.json", "baseline.json",
+                 "dispatcher.c", "dispatcher.py", "bench.csv", "bench.txt"):
+        assert (out / name).exists(), name
+    capsys.readouterr()
+    assert main(["tune", "--config", str(cfg)]) == 0
+    assert "4 already done, 0 to run" in capsys.readouterr().out
+    assert main(["bench", "--config", str(cfg), "--live", "--subset", "all"]) == 0
+
+
+def test_cli_tune_sharded_workers(tmp_path, capsys):
+    from paper_1806_07060_b200.cli import main
+    out = tmp_path / "par"
+    cfg = _config(tmp_path, out, caps={"profile": "b200"})
+    assert main(["tune", "--config", str(cfg), "--gpus", "2"]) == 0
+    tables = sorted(p.name for p in (out / "tables").glob("*.csv"))
+    assert tables == ["16x16x16.csv", "24x24x24.csv", "32x32x32.csv", "8x8x8.csv"]
+    assert main(["tune", "--config", str(cfg), "--gpus", "2", "--force"]) == 0
+    assert "0 already done, 4 to run" in capsys.readouterr().out

@@ -1,0 +1,89 @@
+"""The C-ABI library loads and exports what include/adaptgemm_b200.h declares (CPU only).
+
+No compute call is made here: the CPU container has no GPU.  The host-only
+entry points (legality, registry, workspace sizing, CART, selector) are
+exercised; kernels are checked to exist for every enumerated config.
+"""
+
+import ctypes
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+from paper_1806_07060_b200 import _native, spaces
+from paper_1806_07060_b200.kernels import (
+    DeviceCaps,
+    KernelConfig,
+    KernelFamily,
+    ProblemShape,
+    full_search_space,
+    is_legal,
+    native_shape,
+)
+
+HEADER = ROOT / "include" / "adaptgemm_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(ag_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_loads():
+    lib = _native.lib()
+    assert lib.ag_version().decode().startswith("adaptgemm-b200")
+    assert lib.ag_num_kernels() >= len(spaces.compiled_tuples())
+
+
+def test_every_declared_symbol_is_exported():
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_native.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (ag_[a-z0-9_]+)$", out, re.M))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    # and the ctypes binding covers all of them
+    assert set(syms) <= set(_native.SIGNATURES)
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(_native.LIB_PATH)],
+                         capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.parametrize("caps", [DeviceCaps(), DeviceCaps.b200(), DeviceCaps(register_tile_cap_direct=16),
+                                  DeviceCaps(tile_memory_cap=4096, max_threads=256)])
+def test_native_legality_equals_python(caps):
+    lib = _native.lib()
+    ncaps = caps.native()
+    grid = [(f, bm, bn, bk, tm, tn, uk)
+            for f in (KernelFamily.DIRECT, KernelFamily.INDIRECT)
+            for bm in (8, 16, 24, 64, 256) for bn in (8, 32, 128) for bk in (8, 16, 32)
+            for tm in (1, 2, 3, 8) for tn in (1, 4, 8) for uk in (1, 2)]
+    for t in grid:
+        cfg = KernelConfig(*t)
+        assert bool(lib.ag_is_legal(ctypes.byref(cfg.native()), ctypes.byref(ncaps))) == is_legal(cfg, caps), cfg
+
+
+def test_every_enumerated_config_has_a_kernel():
+    lib = _native.lib()
+    for caps in (DeviceCaps(), DeviceCaps.b200()):
+        for cfg in full_search_space(caps):
+            assert lib.ag_has_kernel(ctypes.byref(cfg.native()), _native.AG_F32), cfg
+            assert lib.ag_has_kernel(ctypes.byref(cfg.native()), _native.AG_F64), cfg
+
+
+def test_workspace_sizes():
+    lib = _native.lib()
+    s = native_shape(ProblemShape(33, 33, 17))
+    d = KernelConfig(KernelFamily.DIRECT, 16, 16, 8, 2, 2, 1)
+    i = KernelConfig(KernelFamily.INDIRECT, 32, 32, 16, 4, 4, 1)
+    assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(d.native()), 0) == 0
+    # Ap: 32 x 64 floats, Bp: 32 x 64 floats, each 256-byte rounded
+    assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(i.native()), 0) == 2 * 32 * 64 * 4
