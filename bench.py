@@ -81,29 +81,32 @@ def build_model():
     db = load_table_bundle(DB_BUNDLE)
     by_shape = {t.shape.mnk: t for t in po2}
     by_shape.update({t.shape.mnk: t for t in db})
-    # training data: po2 train split + DeepBench train split (hybrid), the
-    # tree never sees the held-out shapes it is scored on
-    ds_po2 = dataset_from_tables(po2, "po2")
-    sp_po2 = split(ds_po2, SPLIT_FRACTION, SPLIT_SEED)
-    ds_db = dataset_from_tables(db, "workload")
-    sp_db = split(ds_db, SPLIT_FRACTION, SPLIT_SEED)
-    train_tables = [po2[i] for i in sp_po2.train] + [db[i] for i in sp_db.train]
-    test_tables = [po2[i] for i in sp_po2.test] + [db[i] for i in sp_db.test]
-    ds = dataset_from_tables(train_tables + test_tables, "hybrid")
+    # the reference CLI's "hybrid" dataset (cli.py:166-179): po2 + DeepBench
+    # shapes deduplicated in order, one seeded 80/20 split; the tree is
+    # scored and selected on the held-out 20 % (cmd_train / cmd_eval)
+    hybrid, seen = [], set()
+    for t in po2 + db:
+        if t.shape.mnk not in seen:
+            seen.add(t.shape.mnk)
+            hybrid.append(t)
+    ds = dataset_from_tables(hybrid, "hybrid")
+    sp = split(ds, SPLIT_FRACTION, SPLIT_SEED)
     recs = ds.features_and_labels()
-    n_train = len(train_tables)
-    train_recs, test_recs = recs[:n_train], recs[n_train:]
+    train_recs = [recs[i] for i in sp.train]
+    test_recs = [recs[i] for i in sp.test]
+    test_set = {recs[i][0] for i in sp.test}
+    n_train = len(train_recs)
     named = model.grid_train(train_recs)
     anchor_d, anchor_i = by_shape[(256, 256, 256)], by_shape[(1024, 1024, 1024)]
     policy = evaluation.build_baseline_policy(anchor_d, anchor_i, 384).register(ds.class_index)
-    tables = evaluation.tables_by_shape(train_tables + test_tables)
+    tables = evaluation.tables_by_shape(hybrid)
     scores = evaluation.score_models(named, test_recs, tables, ds.class_index, policy)
     best = evaluation.select_best_model(scores)
     tree = dict(named)[best.name]
     return {
         "tree": tree, "name": best.name, "classes": ds.class_index, "policy": policy,
-        "tables": by_shape, "po2_test": [po2[i].shape for i in sp_po2.test],
-        "db_all": [t.shape for t in db], "db_test": [db[i].shape for i in sp_db.test],
+        "tables": by_shape, "po2_test": [t.shape for t in po2 if t.shape.mnk in test_set],
+        "db_all": [t.shape for t in db], "db_test": [t.shape for t in db if t.shape.mnk in test_set],
         "score": {"accuracy": best.accuracy, "dtpr": best.dtpr, "dttr": best.dttr,
                   "leaves": best.stats.total_leaves, "height": best.stats.height},
         "n_train": n_train, "n_test": len(test_recs),

@@ -276,18 +276,43 @@ tiled_gemm_kernel(const TiledParams<T> p) {
 
     const T* gA = p.At + m0;
     const T* gB = p.Bp + n0;
+    // fixed tiles: chunk loops with compile-time trip counts (fully unrolled,
+    // predicated only when the chunk count is not a multiple of the CTA size)
+    constexpr int NT_C = FIXED ? (BM_ / TM) * (BN_ / TN) : 1;
+    constexpr int CA_C = FIXED ? BK_ * BM_ / VL : 0;
+    constexpr int CB_C = FIXED ? BK_ * BN_ / VL : 0;
     auto load_tile = [&](int kt, int s) {
         const int k0 = kt * BK;
         T* as = As + s * BK * BM;
         T* bs = Bs + s * BK * BN;
-        const int ca = BM / VL, cb = BN / VL;
-        for (int e = tid; e < BK * ca; e += NT) {
-            const int k = e / ca, c = e - k * ca;
-            cp_async<VL * sizeof(T)>(as + k * BM + c * VL, gA + (i64)(k0 + k) * p.lda + c * VL);
-        }
-        for (int e = tid; e < BK * cb; e += NT) {
-            const int k = e / cb, c = e - k * cb;
-            cp_async<VL * sizeof(T)>(bs + k * BN + c * VL, gB + (i64)(k0 + k) * p.ldb + c * VL);
+        if constexpr (FIXED) {
+            constexpr int ca = BM_ / VL, cb = BN_ / VL;
+#pragma unroll
+            for (int it = 0; it < (CA_C + NT_C - 1) / NT_C; ++it) {
+                const int e = tid + it * NT_C;
+                if (CA_C % NT_C == 0 || e < CA_C) {
+                    const int k = e / ca, c = e - k * ca;
+                    cp_async<VL * sizeof(T)>(as + k * BM_ + c * VL, gA + (i64)(k0 + k) * p.lda + c * VL);
+                }
+            }
+#pragma unroll
+            for (int it = 0; it < (CB_C + NT_C - 1) / NT_C; ++it) {
+                const int e = tid + it * NT_C;
+                if (CB_C % NT_C == 0 || e < CB_C) {
+                    const int k = e / cb, c = e - k * cb;
+                    cp_async<VL * sizeof(T)>(bs + k * BN_ + c * VL, gB + (i64)(k0 + k) * p.ldb + c * VL);
+                }
+            }
+        } else {
+            const int ca = BM / VL, cb = BN / VL;
+            for (int e = tid; e < BK * ca; e += NT) {
+                const int k = e / ca, c = e - k * ca;
+                cp_async<VL * sizeof(T)>(as + k * BM + c * VL, gA + (i64)(k0 + k) * p.lda + c * VL);
+            }
+            for (int e = tid; e < BK * cb; e += NT) {
+                const int k = e / cb, c = e - k * cb;
+                cp_async<VL * sizeof(T)>(bs + k * BN + c * VL, gB + (i64)(k0 + k) * p.ldb + c * VL);
+            }
         }
     };
 
