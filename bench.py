@@ -53,7 +53,7 @@ METRIC = "geomean GFLOP/s over GEMM shape set: DT-selected vs oracle vs default 
 # the reference's CPU kernels)
 CPU_DEFAULT_DIRECT = "direct:32-32-16-2-4-1"
 CPU_DEFAULT_INDIRECT = "indirect:64-32-16-4-8-2"
-CPU_SAMPLE_FLOPS = 2.0e8  # per shape per reference step: output rows sized to ~0.1 s
+CPU_SAMPLE_FLOPS = 1.0e8  # per shape per reference step: output rows sized to ~20-50 ms
 
 
 def log(*a):
@@ -265,13 +265,16 @@ def cpu_rates(shapes, budget_flops=CPU_SAMPLE_FLOPS):
     ogemm.build()
     rates = []
     for s in shapes:
-        rows = max(1, min(s.M, int(budget_flops // (2.0 * s.N * s.K))))
-        A, B, C, _ = _bench_buffers(s, np.float32, 0)
-        A = np.ascontiguousarray(A[:rows])
-        C = np.ascontiguousarray(C[:rows])
         canon = CPU_DEFAULT_DIRECT if s.M * s.N * s.K < 384 ** 3 else CPU_DEFAULT_INDIRECT
         fam, params = canon.split(":")
         bm, bn, bk, tm, tn, uk = map(int, params.split("-"))
+        # whole row blocks only, so the sample never pays padding the full
+        # shape would not
+        rows = int(budget_flops // (2.0 * s.N * s.K)) // bm * bm
+        rows = min(s.M, max(bm, rows))
+        A, B, C, _ = _bench_buffers(s, np.float32, 0)
+        A = np.ascontiguousarray(A[:rows])
+        C = np.ascontiguousarray(C[:rows])
         _, sec = ogemm.execute(rows, s.N, s.K, 1.0, 0.0, False, False, A, B, C, fam, bm, bn, bk, tm, tn, uk)
         rates.append(2.0 * rows * s.N * s.K / sec / 1e9)
     return rates, ogemm.num_threads()
@@ -295,8 +298,8 @@ def run_reference(args):
     per_shape = [statistics.median(r[i] for r, _ in per_step) for i in range(len(shapes))]
     value = geomean(per_shape)
     ms = 1e3 * statistics.median(dt for _, dt in per_step)
-    sample = (f"all {len(shapes)} DeepBench-style shapes, each on its first m' output rows with "
-              f"2*m'*N*K ~ {CPU_SAMPLE_FLOPS:.0e} flops; reference CPU default tiles "
+    sample = (f"all {len(shapes)} DeepBench-style shapes, each on its first m' output rows (whole "
+              f"row blocks) with 2*m'*N*K ~ {CPU_SAMPLE_FLOPS:.0e} flops; reference CPU default tiles "
               f"({CPU_DEFAULT_DIRECT} below 384^3, {CPU_DEFAULT_INDIRECT} above)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
@@ -349,6 +352,7 @@ def run_ours(args):
         return runner.pass_(cs, lambda i, c: runner.launch(c, config=nat[i]))
 
     def times(evs):
+        evs[-1][1].synchronize()
         return [e0.elapsed_time(e1) * 1e-3 for e0, e1 in evs]
 
     # warmup (also JITs nothing: the kernels are precompiled sm_100a)

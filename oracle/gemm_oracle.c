@@ -19,8 +19,8 @@
  * of the reference itself in tests/golden/.
  *
  * Parallelism (for the CPU baseline only): OpenMP over independent output
- * row blocks; each output element is still computed by one thread in the
- * reference order, so threading never changes a bit.
+ * tiles (row block x column block); each output element is still computed
+ * by one thread in the reference order, so threading never changes a bit.
  *
  * dtype: 0 float32, 1 float64.  Matrices are row-major with leading dims.
  */
@@ -59,14 +59,15 @@ static int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 void oracle_direct(int64_t M, int64_t N, int64_t K, double alpha, double beta, int ta, int tb, int dt,
                    const void* A, int64_t lda, const void* B, int64_t ldb, const void* C, int64_t ldc,
                    void* out, int64_t ldo, int bm, int bn, int bk, int tm, int tn) {
-    const int64_t nbm = (M + bm - 1) / bm;
+    const int64_t nbm = (M + bm - 1) / bm, nbn = (N + bn - 1) / bn;
 #pragma omp parallel
     {
         double* acc = (double*)malloc(sizeof(double) * (size_t)bm * bn);
 #pragma omp for schedule(dynamic)
-        for (int64_t bi = 0; bi < nbm; ++bi) {
-            const int64_t ii = bi * bm, ih = imin(ii + bm, M);
-            for (int64_t jj = 0; jj < N; jj += bn) {
+        for (int64_t t = 0; t < nbm * nbn; ++t) {
+            const int64_t ii = (t / nbn) * bm, ih = imin(ii + bm, M);
+            {
+                const int64_t jj = (t % nbn) * bn;
                 const int64_t jh = imin(jj + bn, N);
                 for (int64_t i = 0; i < ih - ii; ++i)
                     for (int64_t j = 0; j < jh - jj; ++j) acc[i * bn + j] = 0.0;
@@ -101,14 +102,15 @@ void oracle_direct(int64_t M, int64_t N, int64_t K, double alpha, double beta, i
  * one pairwise term per accumulator update. */
 void oracle_tiled(int64_t Mp, int64_t Np, int64_t Kp, double alpha, double beta, int dt, const void* Ap,
                   const void* Bp, const void* Cp, void* outp, int bm, int bn, int bk, int tm, int tn, int uk) {
-    const int64_t nbm = Mp / bm;
+    const int64_t nbm = Mp / bm, nbn = Np / bn;
 #pragma omp parallel
     {
         double* acc = (double*)malloc(sizeof(double) * (size_t)bm * bn);
 #pragma omp for schedule(dynamic)
-        for (int64_t bi = 0; bi < nbm; ++bi) {
-            const int64_t ii = bi * bm;
-            for (int64_t jj = 0; jj < Np; jj += bn) {
+        for (int64_t t = 0; t < nbm * nbn; ++t) {
+            const int64_t ii = (t / nbn) * bm;
+            {
+                const int64_t jj = (t % nbn) * bn;
                 for (int64_t i = 0; i < (int64_t)bm * bn; ++i) acc[i] = 0.0;
                 for (int64_t kk = 0; kk < Kp; kk += bk)
                     for (int64_t i0 = ii; i0 < ii + bm; i0 += tm)
