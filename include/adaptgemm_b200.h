@@ -39,9 +39,12 @@ extern "C" {
 #define AG_ERR_CUDA 3
 
 /* KernelFamily (kernels.py:32-34).  Values 0/1 match the emitted C
- * dispatcher's `family` field (codegen.py:132). */
+ * dispatcher's `family` field (codegen.py:132).  2 is the B200-profile
+ * split-K family: the indirect core over `uk` equal K slices (unroll_k
+ * carries the slice count) plus a fixed-order reduction -- deterministic. */
 #define AG_FAMILY_DIRECT 0
 #define AG_FAMILY_INDIRECT 1
+#define AG_FAMILY_SPLITK 2
 
 /* element types accepted by gemm_execute (kernels.py:282-283) */
 #define AG_F32 0

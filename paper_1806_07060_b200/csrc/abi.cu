@@ -65,10 +65,17 @@ bool in_range(const ag_config& c) {
            c.bk < 512 && c.tm < 64 && c.tn < 64 && c.uk < 64;
 }
 
-// exact instantiation, else the run-time-tile kernel for (tm, tn)
+// exact instantiation, else the run-time-tile kernel for (tm, tn); the
+// split-K family runs the indirect core (unroll 1) with a K-slice grid axis
 ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
     if (!in_range(c)) return nullptr;
     auto& m = registry().map;
+    if (c.family == AG_FAMILY_SPLITK) {
+        auto it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, 1));
+        if (it != m.end()) return it->second;
+        it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, 0, 0, 0, c.tm, c.tn, 0));
+        return it != m.end() ? it->second : nullptr;
+    }
     auto it = m.find(make_key(c.family, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk));
     if (it != m.end()) return it->second;
     it = m.find(make_key(c.family, dtype, 0, 0, 0, c.tm, c.tn, 0));
@@ -78,8 +85,8 @@ ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
 
 std::string config_str(const ag_config& c) {
     char buf[128];
-    snprintf(buf, sizeof buf, "%s:%d-%d-%d-%d-%d-%d", c.family == AG_FAMILY_DIRECT ? "direct" : "indirect", c.bm, c.bn,
-             c.bk, c.tm, c.tn, c.uk);
+    const char* fam = c.family == AG_FAMILY_DIRECT ? "direct" : (c.family == AG_FAMILY_SPLITK ? "splitk" : "indirect");
+    snprintf(buf, sizeof buf, "%s:%d-%d-%d-%d-%d-%d", fam, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk);
     return buf;
 }
 
@@ -109,6 +116,11 @@ ag::GemmCall make_call(const ag_shape* s, const ag_config* c, int dtype, const v
     g.ws = ws; g.ws_bytes = ws_bytes;
     g.stream = static_cast<cudaStream_t>(stream);
     g.bm = c->bm; g.bn = c->bn; g.bk = c->bk; g.tm = c->tm; g.tn = c->tn; g.uk = c->uk;
+    g.splits = 1;
+    if (c->family == AG_FAMILY_SPLITK) {  // unroll_k carries the number of K slices
+        g.splits = c->uk;
+        g.uk = 1;
+    }
     g.err = &t_err;
     return g;
 }
@@ -257,9 +269,14 @@ const char* ag_version(void) { return "adaptgemm-b200 0.1.0 (sm_100a)"; }
 int ag_is_legal(const ag_config* c, const ag_caps* caps) {
     if (!c || !caps) return 0;
     if (std::min({c->bm, c->bn, c->bk, c->tm, c->tn, c->uk}) < 1) return 0;
-    if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT) return 0;
+    if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT && c->family != AG_FAMILY_SPLITK) return 0;
     if (c->family == AG_FAMILY_DIRECT && c->uk != 1) return 0;
-    if (c->bm % c->tm || c->bn % c->tn || c->bk % c->uk) return 0;
+    if (c->family == AG_FAMILY_SPLITK) {
+        if (c->uk < 2 || c->uk > 64) return 0;  // K slices
+        if (c->bm % c->tm || c->bn % c->tn) return 0;
+    } else if (c->bm % c->tm || c->bn % c->tn || c->bk % c->uk) {
+        return 0;
+    }
     const int64_t cap = c->family == AG_FAMILY_DIRECT ? caps->register_tile_cap_direct : caps->register_tile_cap_indirect;
     if ((int64_t)c->tm * c->tn > cap) return 0;
     if ((int64_t)(c->bm + c->bn) * c->bk * caps->element_size > caps->tile_memory_cap) return 0;
@@ -276,9 +293,10 @@ int ag_has_kernel(const ag_config* c, int dtype) { return c && find_kernel(*c, d
 int ag_num_kernels(void) { return registry().count; }
 
 size_t ag_workspace_bytes(const ag_shape* s, const ag_config* c, int dtype) {
-    if (!s || !c || c->family != AG_FAMILY_INDIRECT || !in_range(*c)) return 0;
-    if (dtype == AG_F64) return ag::indirect_workspace_bytes<double>(s->m, s->n, s->k, c->bm, c->bn, c->bk);
-    return ag::indirect_workspace_bytes<float>(s->m, s->n, s->k, c->bm, c->bn, c->bk);
+    if (!s || !c || c->family == AG_FAMILY_DIRECT || !in_range(*c)) return 0;
+    const int splits = c->family == AG_FAMILY_SPLITK ? c->uk : 1;
+    if (dtype == AG_F64) return ag::indirect_workspace_bytes<double>(s->m, s->n, s->k, c->bm, c->bn, c->bk, splits);
+    return ag::indirect_workspace_bytes<float>(s->m, s->n, s->k, c->bm, c->bn, c->bk, splits);
 }
 
 int ag_gemm(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A, int64_t lda,

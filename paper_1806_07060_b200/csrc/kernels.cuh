@@ -105,6 +105,9 @@ struct TiledParams {
     const T* C; i64 ldc;
     T* out; i64 ldo;
     int bm, bn, bk, uk;
+    int tiles_m, tiles_n, group_m;  // 1-D grid, grouped ("swizzled") tile order
+    int splits, kt_per_split;       // split-K: blockIdx.y is the K slice
+    T* partial;                     // splits x Mp x Np fp partial sums (splits > 1)
 };
 
 // thread bound of a kernel instantiation: exact for fixed tiles; for the
@@ -266,7 +269,19 @@ tiled_gemm_kernel(const TiledParams<T> p) {
 
     const int tid = threadIdx.x;
     const int tx = tid % TX, ty = tid / TX;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    // grouped rasterisation: consecutive CTAs walk group_m row tiles of one
+    // column band, so the band's B tiles and the group's A tiles stay in L2
+    int tm_idx, tn_idx;
+    {
+        const int pid = blockIdx.x;
+        const int per_group = p.group_m * p.tiles_n;
+        const int first_m = (pid / per_group) * p.group_m;
+        const int gsz = min(p.tiles_m - first_m, p.group_m);
+        const int r = pid - (pid / per_group) * per_group;
+        tm_idx = first_m + r % gsz;
+        tn_idx = r / gsz;
+    }
+    const int m0 = tm_idx * BM, n0 = tn_idx * BN;
 
     T acc[TM][TN];
 #pragma unroll
@@ -316,7 +331,11 @@ tiled_gemm_kernel(const TiledParams<T> p) {
         }
     };
 
-    const int nk = p.Kp / BK;
+    // this CTA's K range: all K tiles, or one split-K slice of them
+    const int kt0 = blockIdx.y * p.kt_per_split;
+    const int nk = min(p.Kp / BK - kt0, p.kt_per_split);
+    gA += (i64)kt0 * BK * p.lda;
+    gB += (i64)kt0 * BK * p.ldb;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nk) load_tile(s, s);
@@ -366,6 +385,25 @@ tiled_gemm_kernel(const TiledParams<T> p) {
     }
     cp_async_wait<0>();
 
+    if (p.splits > 1) {
+        // split-K: raw partial sums into this slice's padded Mp x Np slab;
+        // splitk_reduce_kernel adds the slices in order (deterministic)
+        T* slab = p.partial + (i64)blockIdx.y * p.Mp * p.Np;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int gm = m0 + tile_index<WA>(i, ty, TY);
+#pragma unroll
+            for (int g = 0; g < TN / WB; ++g) {
+                const int gn = n0 + g * TX * WB + tx * WB;
+                Vec<T, WB> o;
+#pragma unroll
+                for (int e = 0; e < WB; ++e) o.v[e] = acc[i][g * WB + e];
+                *reinterpret_cast<Vec<T, WB>*>(slab + (i64)gm * p.Np + gn) = o;
+            }
+        }
+        return;
+    }
+
     // masked store epilogue (replaces outp + unpad copy, kernels.py:322-325)
     const bool full = (m0 + BM <= p.M) && (n0 + BN <= p.N);
     if (full && p.vec_out) {
@@ -401,6 +439,22 @@ tiled_gemm_kernel(const TiledParams<T> p) {
                 p.out[(i64)gm * p.ldo + gn] = v;
             }
         }
+    }
+}
+
+// out = alpha * (sum over slices z = 0..splits-1, in order) + beta * C
+// (C only when use_c): the fixed-order reduction of the split-K family
+template <typename T>
+__global__ void __launch_bounds__(256)
+splitk_reduce_kernel(const T* __restrict__ partial, int splits, i64 slab, int Np, int M, int N, T alpha, T beta,
+                     int use_c, const T* __restrict__ C, i64 ldc, T* __restrict__ out, i64 ldo) {
+    const i64 total = (i64)M * N;
+    for (i64 idx = (i64)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+        const int m = (int)(idx / N), n = (int)(idx - (i64)m * N);
+        const T* src = partial + (i64)m * Np + n;
+        T sum = src[0];
+        for (int z = 1; z < splits; ++z) sum += src[z * slab];
+        out[(i64)m * ldo + n] = use_c ? fmadd(alpha, sum, beta * C[(i64)m * ldc + n]) : alpha * sum;
     }
 }
 

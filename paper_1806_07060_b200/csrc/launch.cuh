@@ -7,6 +7,7 @@
 //              16-byte aligned matrix in the layout the core streams
 //              (CLBlast-style "helpers only when needed").
 #pragma once
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <string>
@@ -74,11 +75,17 @@ int launch_direct(const GemmCall& c) {
     return cudaGetLastError() == cudaSuccess ? AG_OK : fail(c, AG_ERR_CUDA, "direct kernel launch failed");
 }
 
+// [At | Bp | split-K partial slabs], each 256-byte aligned
 template <typename T>
-size_t indirect_workspace_bytes(i64 M, i64 N, i64 K, int bm, int bn, int bk) {
+size_t indirect_workspace_bytes(i64 M, i64 N, i64 K, int bm, int bn, int bk, int splits = 1) {
     const i64 Mp = round_up(M, bm), Np = round_up(N, bn), Kp = round_up(K, bk);
-    return (size_t)round_up(Kp * Mp * (i64)sizeof(T), 256) + (size_t)round_up(Kp * Np * (i64)sizeof(T), 256);
+    size_t b = (size_t)round_up(Kp * Mp * (i64)sizeof(T), 256) + (size_t)round_up(Kp * Np * (i64)sizeof(T), 256);
+    if (splits > 1) b += (size_t)round_up((i64)splits * Mp * Np * (i64)sizeof(T), 256);
+    return b;
 }
+
+// L2-friendly tile grouping: ~8 row tiles per group (CUTLASS-style swizzle)
+inline int group_rows(i64 tiles_m) { return (int)(tiles_m < 8 ? tiles_m : 8); }
 
 template <typename T, int BM, int BN, int BK, int TM, int TN, int UK>
 int launch_indirect(const GemmCall& c) {
@@ -102,9 +109,15 @@ int launch_indirect(const GemmCall& c) {
     const i64 Mp = round_up(M, bm), Np = round_up(N, bn), Kp = round_up(K, bk);
     if (Mp / bm > 65535) return fail(c, AG_ERR_SHAPE, "problem too large for the indirect grid");
     if (Mp > 0x7fffffff || Np > 0x7fffffff || Kp > 0x7fffffff) return fail(c, AG_ERR_SHAPE, "dimension too large");
-    const size_t need = indirect_workspace_bytes<T>(M, N, K, bm, bn, bk);
+    const int splits = c.splits > 1 ? c.splits : 1;
+    const size_t need = indirect_workspace_bytes<T>(M, N, K, bm, bn, bk, splits);
     if (c.ws_bytes < need || (need && c.ws == nullptr))
         return fail(c, AG_ERR_SHAPE, "workspace too small for the indirect pack buffers");
+    const i64 tiles_m = Mp / bm, tiles_n = Np / bn, ktiles = Kp / bk;
+    if (tiles_m * tiles_n > 0x7fffffffLL) return fail(c, AG_ERR_SHAPE, "too many tiles");
+    // split-K: equal K-tile slices; splits beyond the K tiles collapse
+    const int kps = (int)((ktiles + splits - 1) / splits);
+    const int used_splits = (int)((ktiles + kps - 1) / kps);
     const size_t va = VL * sizeof(T);
 
     // op(A)^T, K-major (Kp x Mp): A itself when transA and already padded
@@ -144,8 +157,21 @@ int launch_indirect(const GemmCall& c) {
     p.C = static_cast<const T*>(c.C); p.ldc = c.ldc;
     p.out = static_cast<T*>(c.out); p.ldo = c.ldo;
     p.bm = bm; p.bn = bn; p.bk = bk; p.uk = uk;
-    kernel<<<dim3((unsigned)(Np / bn), (unsigned)(Mp / bm)), threads, smem, c.stream>>>(p);
-    return cudaGetLastError() == cudaSuccess ? AG_OK : fail(c, AG_ERR_CUDA, "indirect kernel launch failed");
+    p.tiles_m = (int)tiles_m; p.tiles_n = (int)tiles_n; p.group_m = group_rows(tiles_m);
+    p.splits = used_splits; p.kt_per_split = kps;
+    p.partial = reinterpret_cast<T*>(static_cast<char*>(c.ws) + round_up(Kp * Mp * (i64)sizeof(T), 256) +
+                                     round_up(Kp * Np * (i64)sizeof(T), 256));
+    kernel<<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)used_splits), threads, smem, c.stream>>>(p);
+    if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "indirect kernel launch failed");
+    if (used_splits > 1) {
+        const i64 total = M * N;
+        const unsigned blocks = (unsigned)std::min<i64>((total + 255) / 256, 148 * 16);
+        splitk_reduce_kernel<T><<<blocks, 256, 0, c.stream>>>(p.partial, used_splits, Mp * Np, (int)Np, (int)M,
+                                                               (int)N, p.alpha, p.beta, p.use_c, p.C, c.ldc, p.out,
+                                                               c.ldo);
+        if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "split-K reduce launch failed");
+    }
+    return AG_OK;
 }
 
 }  // namespace ag

@@ -22,6 +22,7 @@ struct GemmCall {
     void* ws; size_t ws_bytes;
     cudaStream_t stream;
     int bm, bn, bk, tm, tn, uk;  // run-time tile sizes (run-time-tile kernels)
+    int splits;                  // split-K slices (splitk family); 1 otherwise
     std::string* err;
 };
 

@@ -36,12 +36,24 @@ class ConfigError(ValueError):
 
 
 class KernelFamily(str, Enum):
+    """The reference's two families plus the B200-profile split-K family.
+
+    SPLITK runs the indirect core over `unroll_k` equal K slices and adds
+    the slices in a fixed order (deterministic); it exists only in the B200
+    profile, so reference-profile spaces, tables and dispatchers are
+    unchanged.
+    """
+
     DIRECT = "direct"
     INDIRECT = "indirect"
+    SPLITK = "splitk"
 
 
+REFERENCE_FAMILIES = (KernelFamily.DIRECT, KernelFamily.INDIRECT)
 _FAMILY_CODE = {KernelFamily.DIRECT: _native.AG_FAMILY_DIRECT,
-                KernelFamily.INDIRECT: _native.AG_FAMILY_INDIRECT}
+                KernelFamily.INDIRECT: _native.AG_FAMILY_INDIRECT,
+                KernelFamily.SPLITK: _native.AG_FAMILY_SPLITK}
+_CODE_FAMILY = {v: k for k, v in _FAMILY_CODE.items()}
 
 
 @dataclass(frozen=True)
@@ -107,7 +119,7 @@ class DeviceCaps:
     def register_tile_cap(self, family: KernelFamily) -> int:
         if family is KernelFamily.DIRECT:
             return self.register_tile_cap_direct
-        return self.register_tile_cap_indirect
+        return self.register_tile_cap_indirect  # indirect and split-K
 
     def as_dict(self) -> dict:
         return dict(tile_memory_cap=self.tile_memory_cap,
@@ -162,8 +174,11 @@ class KernelConfig:
 
     @classmethod
     def from_native(cls, c: _native.AgConfig) -> "KernelConfig":
-        fam = KernelFamily.DIRECT if c.family == _native.AG_FAMILY_DIRECT else KernelFamily.INDIRECT
-        return cls(fam, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk)
+        return cls(_CODE_FAMILY[c.family], c.bm, c.bn, c.bk, c.tm, c.tn, c.uk)
+
+    @property
+    def family_code(self) -> int:
+        return _FAMILY_CODE[self.family]
 
 
 # Parameter domains for exhaustive enumeration, in canonical order (kernels.py:123-138)
@@ -172,6 +187,13 @@ INDIRECT_DOMAINS = spaces.INDIRECT_DOMAINS
 
 
 def domains_for(family: KernelFamily) -> dict[str, tuple[int, ...]]:
+    if family is KernelFamily.SPLITK:
+        return {"block_m": tuple(sorted({t[0] for t in spaces.SPLITK_TILES})),
+                "block_n": tuple(sorted({t[1] for t in spaces.SPLITK_TILES})),
+                "block_k": spaces.SPLITK_BLOCK_K,
+                "tile_m": tuple(sorted({t[2] for t in spaces.SPLITK_TILES})),
+                "tile_n": tuple(sorted({t[3] for t in spaces.SPLITK_TILES})),
+                "unroll_k": spaces.SPLITK_SLICES}
     return DIRECT_DOMAINS if family is KernelFamily.DIRECT else INDIRECT_DOMAINS
 
 
@@ -192,9 +214,12 @@ def enumerate_search_space(family: KernelFamily, caps: DeviceCaps = DeviceCaps()
 
 
 def full_search_space(caps: DeviceCaps = DeviceCaps()) -> list[KernelConfig]:
-    """Both families concatenated: direct block first, then indirect."""
-    return (enumerate_search_space(KernelFamily.DIRECT, caps)
-            + enumerate_search_space(KernelFamily.INDIRECT, caps))
+    """All families concatenated: direct block first, then indirect (then, in
+    the B200 profile only, split-K)."""
+    out = []
+    for fam in KernelFamily:
+        out.extend(enumerate_search_space(fam, caps))
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -42,6 +42,17 @@ B200_INDIRECT_EXTRA_DOMAINS = {
     "unroll_k": (1, 2),
 }
 
+# B200 profile, split-K family ("splitk"): the indirect core over `uk` equal
+# K slices plus a fixed-order reduction.  For skinny / small-N shapes whose
+# tile grid cannot fill 148 SMs.  Tiles are ones the indirect family already
+# compiles (unroll 1), so the family adds no instantiations.
+SPLITK_TILES = ((16, 16, 2, 2), (32, 16, 4, 2), (16, 32, 2, 4), (32, 32, 4, 4), (64, 16, 4, 2),
+                (16, 64, 2, 4), (64, 32, 4, 4), (32, 64, 4, 4), (64, 64, 8, 4), (64, 64, 4, 8),
+                (128, 64, 8, 4), (64, 128, 4, 8), (128, 64, 8, 8), (64, 128, 8, 8), (128, 128, 8, 8))
+SPLITK_BLOCK_K = (16, 32)
+SPLITK_SLICES = (2, 4, 8, 16)
+FAMILIES = ("direct", "indirect", "splitk")
+
 PROFILE_REFERENCE = "reference"
 PROFILE_B200 = "b200"
 
@@ -67,9 +78,16 @@ def is_legal_tuple(family, bm, bn, bk, tm, tn, uk, caps) -> bool:
     """
     if min(bm, bn, bk, tm, tn, uk) < 1:
         return False
+    if family not in FAMILIES:
+        return False
     if family == "direct" and uk != 1:
         return False
-    if bm % tm or bn % tn or bk % uk:
+    if family == "splitk":
+        if not 2 <= uk <= 64:  # uk carries the number of K slices
+            return False
+        if bm % tm or bn % tn:
+            return False
+    elif bm % tm or bn % tn or bk % uk:
         return False
     cap = caps["register_tile_cap_direct"] if family == "direct" else caps["register_tile_cap_indirect"]
     if tm * tn > cap:
@@ -91,6 +109,11 @@ def _product(family, domains):
 
 def enumerate_tuples(family, caps, profile=PROFILE_REFERENCE):
     """Legal configs of one family in deterministic canonical order."""
+    if family == "splitk":
+        if profile != PROFILE_B200:
+            return []
+        return [t for (bm, bn, tm, tn) in SPLITK_TILES for bk in SPLITK_BLOCK_K for s in SPLITK_SLICES
+                for t in [("splitk", bm, bn, bk, tm, tn, s)] if is_legal_tuple(*t, caps)]
     base = DIRECT_DOMAINS if family == "direct" else INDIRECT_DOMAINS
     out = [t for t in _product(family, base) if is_legal_tuple(*t, caps)]
     if profile == PROFILE_B200 and family == "indirect":

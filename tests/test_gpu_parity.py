@@ -121,7 +121,7 @@ def test_randomized_c1_generator(search_space):
     """The reference acceptance C1 generator (test_acceptance.py:78-111): 200
     shapes x 20 configs per family, vs the bit-exact CPU oracle."""
     stream = rng.SplitMix64(0xC1)
-    fams = {f: [c for c in search_space if c.family is f] for f in KernelFamily}
+    fams = {f: [c for c in search_space if c.family is f] for f in (KernelFamily.DIRECT, KernelFamily.INDIRECT)}
     for case in range(200):
         s = ProblemShape(1 + stream.below(96), 1 + stream.below(96), 1 + stream.below(96),
                          alpha=(1.0, 1.5, 2.0)[stream.below(3)], beta=(0.0, 0.0, 0.5, 1.0)[stream.below(4)],
@@ -248,3 +248,46 @@ def test_full_size_properties(mnk, cfg):
     o1, _ = gemm_execute(s, config, dA, dB, dC, B200)
     o2, _ = gemm_execute(s, config, dA, dB * 2, dC, B200)
     assert torch.equal(o2, o1 * 2)
+
+
+# ---------------------------------------------------------------------------
+# split-K family (B200 profile)
+
+
+@pytest.mark.parametrize("ta,tb", list(itertools.product([False, True], repeat=2)))
+def test_splitk_parity_and_determinism(ta, tb):
+    s = ProblemShape(70, 33, 1000, alpha=1.25, beta=0.75, transA=ta, transB=tb)
+    A, B, C = rand_operands(s, seed=29)
+    ref = _oracle_ref(s, A, B, C)
+    for canon in ("splitk:16-16-16-2-2-2", "splitk:32-32-32-4-4-8", "splitk:64-64-32-8-4-16",
+                  "splitk:128-64-16-8-8-4"):
+        cfg = KernelConfig.from_canonical(canon)
+        out1, _ = gemm_execute(s, cfg, A, B, C, B200)
+        out2, _ = gemm_execute(s, cfg, A, B, C, B200)
+        assert_rf(out1, ref)
+        np.testing.assert_array_equal(out1, out2)  # fixed-order reduction: bitwise repeatable
+
+
+def test_splitk_more_slices_than_k_tiles():
+    s = ProblemShape(40, 40, 20, beta=0.5)  # 2 K tiles of 16, 16 slices requested
+    A, B, C = rand_operands(s, seed=30)
+    out, _ = gemm_execute(s, KernelConfig.from_canonical("splitk:16-16-16-2-2-16"), A, B, C, B200)
+    assert_rf(out, _oracle_ref(s, A, B, C))
+
+
+def test_splitk_illegal_under_reference_caps():
+    s = ProblemShape(8, 8, 8)
+    A, B, C = rand_operands(s)
+    with pytest.raises(ConfigError):
+        gemm_execute(s, KernelConfig.from_canonical("splitk:16-16-16-2-2-1"), A, B, C, B200)  # 1 slice
+
+
+@pytest.mark.parametrize("mnk", [(4096, 16, 4096), (2048, 32, 2048), (35, 700, 2560)])
+def test_splitk_full_size_skinny(mnk):
+    s = ProblemShape(*mnk)
+    A, B, C = rand_operands(s, seed=3)
+    out, _ = gemm_execute(s, KernelConfig.from_canonical("splitk:32-16-32-4-2-16"), A, B, C, B200)
+    assert _checksum_ok(s, A, B, C, out)
+    rows = np.array(rng.sample_without_replacement(s.M, min(16, s.M), 9))
+    exact = A[rows].astype(np.float64) @ B.astype(np.float64)
+    assert rel_frobenius(out[rows], exact) <= 1e-5
