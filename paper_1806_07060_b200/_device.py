@@ -91,9 +91,17 @@ def current_stream_handle(device) -> int:
     return int(t.cuda.current_stream(device).cuda_stream)
 
 
-def to_device(a: np.ndarray, device):
-    """Copy a numpy matrix to a contiguous device tensor."""
+def is_cuda_tensor(x) -> bool:
+    return is_device_tensor(x) and x.is_cuda
+
+
+def to_device(a, device):
+    """Copy a host matrix (numpy array or torch CPU tensor) to a contiguous
+    device tensor; pinned torch tensors are copied asynchronously."""
     t = torch()
+    if is_device_tensor(a):
+        src = a.contiguous()
+        return src.to(device=device, non_blocking=bool(src.is_pinned()))
     src = t.from_numpy(np.ascontiguousarray(a))
     return src.to(device=device, non_blocking=False)
 

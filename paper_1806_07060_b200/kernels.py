@@ -251,24 +251,29 @@ def _check_operands(shape: ProblemShape, A, B, C):
 
 
 class _Operands:
-    """Device views of (A, B, C, out) for one call, host or device side."""
+    """Device views of (A, B, C, out) for one call, host or device side.
 
-    def __init__(self, shape: ProblemShape, A, B, C, out):
-        self.host = not any(_device.is_device_tensor(x) for x in (A, B, C))
+    Host operands are numpy arrays or torch CPU tensors (pinned ones move
+    asynchronously).  `need_c=False` (beta == 0 with a family that never
+    reads C) skips staging C; the kernel then gets `out` as a never-read C.
+    """
+
+    def __init__(self, shape: ProblemShape, A, B, C, out, need_c: bool = True):
+        self.host = not any(_device.is_cuda_tensor(x) for x in (A, B, C))
         t = _device.require_cuda()
         self.code = _device.dtype_code(A.dtype)
         if self.host:
-            if out is not None and (_dims(out) != (shape.M, shape.N) or out.dtype != A.dtype):
+            if out is not None and (_dims(out) != (shape.M, shape.N) or _device.dtype_code(out.dtype) != self.code):
                 raise ShapeError("out buffer has wrong shape or dtype")
             self.device = _device.default_device()
             self.A = _device.to_device(A, self.device)
             self.B = _device.to_device(B, self.device)
-            self.C = _device.to_device(C, self.device)
             self.out_host = out
             self.out = t.empty((shape.M, shape.N), dtype=self.A.dtype, device=self.device)
+            self.C = _device.to_device(C, self.device) if need_c else self.out
         else:
             for name, x in (("A", A), ("B", B), ("C", C)):
-                if not _device.is_device_tensor(x) or not x.is_cuda:
+                if not _device.is_cuda_tensor(x):
                     raise ShapeError(f"{name} must be a CUDA tensor when any operand is one")
             self.device = A.device
             if B.device != self.device or C.device != self.device:
@@ -295,10 +300,15 @@ class _Operands:
 
     def result(self):
         if self.host:
+            out = self.out_host
+            if out is not None and _device.is_device_tensor(out):  # torch CPU (pinned: async D2H)
+                out.copy_(self.out, non_blocking=bool(out.is_pinned()))
+                _device.torch().cuda.current_stream(self.device).synchronize()
+                return out
             res = self.out.cpu().numpy()
-            if self.out_host is not None:
-                self.out_host[...] = res
-                return self.out_host
+            if out is not None:
+                out[...] = res
+                return out
             return res
         if self.out is not self.out_user:
             self.out_user.copy_(self.out)
@@ -317,6 +327,12 @@ def _raise_for(code: int, config: "KernelConfig | None" = None):
 def native_shape(shape: ProblemShape) -> _native.AgShape:
     return _native.AgShape(shape.M, shape.N, shape.K, float(shape.alpha), float(shape.beta),
                            int(bool(shape.transA)), int(bool(shape.transB)))
+
+
+def reads_c(shape: ProblemShape, config: KernelConfig) -> bool:
+    """Whether the family path reads C: always for direct (kernels.py:227),
+    only when beta != 0 for indirect / split-K (kernels.py:318-321)."""
+    return config.family is KernelFamily.DIRECT or shape.beta != 0.0
 
 
 def workspace_bytes(shape: ProblemShape, config: KernelConfig, dtype=np.float32) -> int:
@@ -410,7 +426,7 @@ def gemm_execute(shape: ProblemShape, config: KernelConfig, A, B, C,
     if not is_legal(config, caps):
         raise ConfigError(f"illegal config {config.canonical()} for caps {caps}")
     _check_operands(shape, A, B, C)
-    ops = _Operands(shape, A, B, C, out)
+    ops = _Operands(shape, A, B, C, out, need_c=reads_c(shape, config))
     elapsed = _launch(shape, config, caps, ops, timed=True)
     return ops.result(), max(elapsed, 1e-9)
 
