@@ -71,7 +71,9 @@ ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
     if (!in_range(c)) return nullptr;
     auto& m = registry().map;
     if (c.family == AG_FAMILY_SPLITK) {
-        auto it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, 1));
+        auto it = m.find(make_key(AG_FAMILY_SPLITK, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, 0));
+        if (it != m.end()) return it->second;
+        it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, 1));
         if (it != m.end()) return it->second;
         it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, 0, 0, 0, c.tm, c.tn, 0));
         return it != m.end() ? it->second : nullptr;

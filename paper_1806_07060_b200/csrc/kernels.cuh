@@ -251,10 +251,20 @@ direct_gemm_kernel(const DirectParams<T> p) {
 // ---------------------------------------------------------------------------
 // indirect family: unpredicated multi-stage core on packed operands
 // ---------------------------------------------------------------------------
-template <typename T, int BM_, int BN_, int BK_, int TM, int TN, int UK, int STAGES>
+// AROW: A is read straight from the caller's row-major M x K operand (no
+// transpose-pack) with 4-byte copies transposed into the K-major tile; the
+// A tile rows are padded by 4 elements to spread the transposing writes
+// over the banks.  Used by the split-K family when M and K are tile
+// multiples -- skinny memory-bound shapes, where the pack would double the
+// A traffic.
+template <typename T, bool AROW>
+__host__ __device__ constexpr int a_pad() { return AROW ? 4 : 0; }
+
+template <typename T, int BM_, int BN_, int BK_, int TM, int TN, int UK, int STAGES, bool AROW = false>
 __global__ void __launch_bounds__(cta_threads_bound<T, BM_, BN_, TM, TN>())
 tiled_gemm_kernel(const TiledParams<T> p) {
     constexpr bool FIXED = BM_ > 0 && BN_ > 0 && BK_ > 0;
+    static_assert(!AROW || FIXED, "row-major A needs fixed tiles");
     constexpr int VL = FIXED ? VecW<T>::W : 1;  // elements per cp.async
     constexpr int WA = FragW<T, TM>::W;
     constexpr int WB = FragW<T, TN>::W;
@@ -262,10 +272,11 @@ tiled_gemm_kernel(const TiledParams<T> p) {
     const int BN = FIXED ? BN_ : p.bn;
     const int BK = FIXED ? BK_ : p.bk;
     const int TX = BN / TN, TY = BM / TM, NT = TX * TY;
+    const int LA = BM + a_pad<T, AROW>();  // A tile row stride (elements)
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* As = reinterpret_cast<T*>(smem_raw);  // [STAGES][BK][BM]
-    T* Bs = As + STAGES * BK * BM;            // [STAGES][BK][BN]
+    T* As = reinterpret_cast<T*>(smem_raw);  // [STAGES][BK][LA]
+    T* Bs = As + STAGES * BK * LA;            // [STAGES][BK][BN]
 
     const int tid = threadIdx.x;
     const int tx = tid % TX, ty = tid / TX;
@@ -289,21 +300,37 @@ tiled_gemm_kernel(const TiledParams<T> p) {
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
 
-    const T* gA = p.At + m0;
+    // K-major packed A: row k of the tile is contiguous; row-major A (AROW):
+    // row i of the tile is contiguous along k
+    const T* gA = AROW ? p.At + (i64)m0 * p.lda : p.At + m0;
     const T* gB = p.Bp + n0;
     // fixed tiles: chunk loops with compile-time trip counts (fully unrolled,
     // predicated only when the chunk count is not a multiple of the CTA size)
     constexpr int NT_C = FIXED ? (BM_ / TM) * (BN_ / TN) : 1;
     constexpr int CA_C = FIXED ? BK_ * BM_ / VL : 0;
     constexpr int CB_C = FIXED ? BK_ * BN_ / VL : 0;
+    constexpr int LA_C = BM_ + a_pad<T, AROW>();
     auto load_tile = [&](int kt, int s) {
         const int k0 = kt * BK;
-        T* as = As + s * BK * BM;
+        T* as = As + s * BK * LA;
         T* bs = Bs + s * BK * BN;
+        if constexpr (FIXED && AROW) {
+            // element copies, k fastest (coalesced rows), transposed into As[k][i]
+            constexpr int EA = BK_ * BM_;
+#pragma unroll
+            for (int it = 0; it < (EA + NT_C - 1) / NT_C; ++it) {
+                const int e = tid + it * NT_C;
+                if (EA % NT_C == 0 || e < EA) {
+                    const int k = e % BK_, i = e / BK_;
+                    cp_async<sizeof(T)>(as + k * LA_C + i, gA + (i64)i * p.lda + k0 + k);
+                }
+            }
+        }
         if constexpr (FIXED) {
             constexpr int ca = BM_ / VL, cb = BN_ / VL;
 #pragma unroll
             for (int it = 0; it < (CA_C + NT_C - 1) / NT_C; ++it) {
+                if constexpr (AROW) break;
                 const int e = tid + it * NT_C;
                 if (CA_C % NT_C == 0 || e < CA_C) {
                     const int k = e / ca, c = e - k * ca;
@@ -334,7 +361,7 @@ tiled_gemm_kernel(const TiledParams<T> p) {
     // this CTA's K range: all K tiles, or one split-K slice of them
     const int kt0 = blockIdx.y * p.kt_per_split;
     const int nk = min(p.Kp / BK - kt0, p.kt_per_split);
-    gA += (i64)kt0 * BK * p.lda;
+    gA += AROW ? (i64)kt0 * BK : (i64)kt0 * BK * p.lda;
     gB += (i64)kt0 * BK * p.ldb;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -351,7 +378,7 @@ tiled_gemm_kernel(const TiledParams<T> p) {
             cp_async_commit();
         }
         const int s = kt % STAGES;
-        const T* as = As + s * BK * BM;
+        const T* as = As + s * BK * LA;
         const T* bs = Bs + s * BK * BN;
         if (FIXED) {
 #pragma unroll
@@ -359,7 +386,7 @@ tiled_gemm_kernel(const TiledParams<T> p) {
                 T a[UK][TM], b[UK][TN];
 #pragma unroll
                 for (int u = 0; u < UK; ++u) {
-                    load_frag<T, TM, WA>(a[u], as + (k + u) * BM, ty, TY);
+                    load_frag<T, TM, WA>(a[u], as + (k + u) * LA_C, ty, TY);
                     load_frag<T, TN, WB>(b[u], bs + (k + u) * BN, tx, TX);
                 }
 #pragma unroll

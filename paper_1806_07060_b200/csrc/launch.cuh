@@ -87,10 +87,14 @@ size_t indirect_workspace_bytes(i64 M, i64 N, i64 K, int bm, int bn, int bk, int
 // L2-friendly tile grouping: ~8 row tiles per group (CUTLASS-style swizzle)
 inline int group_rows(i64 tiles_m) { return (int)(tiles_m < 8 ? tiles_m : 8); }
 
-template <typename T, int BM, int BN, int BK, int TM, int TN, int UK>
+// AROW_OK (split-K family launchers): when op(A) is the caller's row-major
+// A and M, K are tile multiples, run the AROW core that reads A in place
+// instead of transpose-packing it.
+template <typename T, int BM, int BN, int BK, int TM, int TN, int UK, bool AROW_OK = false>
 int launch_indirect(const GemmCall& c) {
     constexpr bool FIXED = BM > 0 && BN > 0 && BK > 0;
     constexpr int STAGES = tiled_stages<T>(BM, BN, BK);
+    constexpr int STAGES_AROW = tiled_stages<T>(BM + a_pad<T, true>(), BN, BK);
     constexpr int VL = FIXED ? VecW<T>::W : 1;
     constexpr int WB = FragW<T, TN>::W;
     const int bm = FIXED ? BM : c.bm, bn = FIXED ? BN : c.bn, bk = FIXED ? BK : c.bk;
@@ -99,15 +103,24 @@ int launch_indirect(const GemmCall& c) {
     if (threads > cta_threads_bound<T, BM, BN, TM, TN>())
         return fail(c, AG_ERR_CONFIG, "config needs more threads per CTA than its kernel supports");
     if (bk % uk) return fail(c, AG_ERR_CONFIG, "block_k must be a multiple of unroll_k");
-    const size_t smem = tiled_smem_bytes<T>(bm, bn, bk, STAGES);
+    const i64 M = c.M, N = c.N, K = c.K;
+    const bool arow = FIXED && AROW_OK && !c.ta && M % bm == 0 && K % bk == 0;
+    const size_t smem = arow ? tiled_smem_bytes<T>(bm + a_pad<T, true>(), bn, bk, STAGES_AROW)
+                             : tiled_smem_bytes<T>(bm, bn, bk, STAGES);
     if (smem > 227 * 1024) return fail(c, AG_ERR_CONFIG, "config exceeds 227 KB shared memory per CTA");
     auto kernel = tiled_gemm_kernel<T, BM, BN, BK, TM, TN, UK, STAGES>;
     static std::atomic<size_t> granted{0};
-    if (ensure_smem(kernel, smem, granted) != cudaSuccess) return fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
+    cudaError_t attr = cudaSuccess;
+    if constexpr (AROW_OK && FIXED) {
+        static std::atomic<size_t> granted_arow{0};
+        attr = arow ? ensure_smem(tiled_gemm_kernel<T, BM, BN, BK, TM, TN, UK, STAGES_AROW, true>, smem, granted_arow)
+                    : ensure_smem(kernel, smem, granted);
+    } else {
+        attr = ensure_smem(kernel, smem, granted);
+    }
+    if (attr != cudaSuccess) return fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
 
-    const i64 M = c.M, N = c.N, K = c.K;
     const i64 Mp = round_up(M, bm), Np = round_up(N, bn), Kp = round_up(K, bk);
-    if (Mp / bm > 65535) return fail(c, AG_ERR_SHAPE, "problem too large for the indirect grid");
     if (Mp > 0x7fffffff || Np > 0x7fffffff || Kp > 0x7fffffff) return fail(c, AG_ERR_SHAPE, "dimension too large");
     const int splits = c.splits > 1 ? c.splits : 1;
     const size_t need = indirect_workspace_bytes<T>(M, N, K, bm, bn, bk, splits);
@@ -125,7 +138,10 @@ int launch_indirect(const GemmCall& c) {
     i64 lda_t;
     T* wsA = static_cast<T*>(c.ws);
     T* wsB = reinterpret_cast<T*>(static_cast<char*>(c.ws) + round_up(Kp * Mp * (i64)sizeof(T), 256));
-    if (c.ta && M == Mp && K == Kp && c.lda % VL == 0 && aligned(c.A, va)) {
+    if (arow) {  // row-major A read in place by the AROW core
+        At = static_cast<const T*>(c.A);
+        lda_t = c.lda;
+    } else if (c.ta && M == Mp && K == Kp && c.lda % VL == 0 && aligned(c.A, va)) {
         At = static_cast<const T*>(c.A);
         lda_t = c.lda;
     } else {
@@ -161,7 +177,15 @@ int launch_indirect(const GemmCall& c) {
     p.splits = used_splits; p.kt_per_split = kps;
     p.partial = reinterpret_cast<T*>(static_cast<char*>(c.ws) + round_up(Kp * Mp * (i64)sizeof(T), 256) +
                                      round_up(Kp * Np * (i64)sizeof(T), 256));
-    kernel<<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)used_splits), threads, smem, c.stream>>>(p);
+    const dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)used_splits);
+    bool launched = false;
+    if constexpr (AROW_OK && FIXED) {
+        if (arow) {
+            tiled_gemm_kernel<T, BM, BN, BK, TM, TN, UK, STAGES_AROW, true><<<grid, threads, smem, c.stream>>>(p);
+            launched = true;
+        }
+    }
+    if (!launched) kernel<<<grid, threads, smem, c.stream>>>(p);
     if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "indirect kernel launch failed");
     if (used_splits > 1) {
         const i64 total = M * N;

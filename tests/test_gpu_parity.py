@@ -291,3 +291,16 @@ def test_splitk_full_size_skinny(mnk):
     rows = np.array(rng.sample_without_replacement(s.M, min(16, s.M), 9))
     exact = A[rows].astype(np.float64) @ B.astype(np.float64)
     assert rel_frobenius(out[rows], exact) <= 1e-5
+
+
+@pytest.mark.parametrize("canon", ["splitk:32-16-32-4-2-16", "splitk:64-64-16-8-4-8", "splitk:128-128-32-8-8-2"])
+def test_splitk_row_major_a_path(canon):
+    """Aligned M, K with row-major A: split-K reads A in place (no pack)."""
+    cfg = KernelConfig.from_canonical(canon)
+    s = ProblemShape(4 * cfg.block_m, 48, 8 * cfg.block_k, alpha=0.5, beta=1.5, transB=True)
+    A, B, C = rand_operands(s, seed=41)
+    ref = _oracle_ref(s, A, B, C)
+    out1, _ = gemm_execute(s, cfg, A, B, C, B200)
+    out2, _ = gemm_execute(s, cfg, A, B, C, B200)
+    assert_rf(out1, ref)
+    np.testing.assert_array_equal(out1, out2)
