@@ -45,6 +45,14 @@ extern "C" {
 #define AG_FAMILY_DIRECT 0
 #define AG_FAMILY_INDIRECT 1
 #define AG_FAMILY_SPLITK 2
+/* 3, 4: the B200 tensor-core families (tcgen05.mma with TMEM accumulators,
+ * TMA-fed): float32 operands packed to tf32 (round to nearest) or bf16
+ * (round to nearest even), fp32 accumulation.  No reference analogue; they
+ * enter only the "b200tc" search space (BASELINE.json configs[4]).
+ * bm = 128 (UMMA M), bn = UMMA N, bk = one 128-byte K block (32 tf32 /
+ * 64 bf16 elements), tm = shared-memory pipeline stages, tn = uk = 1. */
+#define AG_FAMILY_TF32 3
+#define AG_FAMILY_BF16 4
 
 /* element types accepted by gemm_execute (kernels.py:282-283) */
 #define AG_F32 0
@@ -90,7 +98,8 @@ int ag_has_kernel(const ag_config* config, int dtype);
 int ag_num_kernels(void);
 
 /* bytes of device workspace one gemm call needs (pack buffers of the
- * indirect family, kernels.py:304-322); 0 for the direct family */
+ * indirect family, kernels.py:304-322, and of the tensor-core families);
+ * 0 for the direct family */
 size_t ag_workspace_bytes(const ag_shape* shape, const ag_config* config, int dtype);
 
 /* ------------------------------------------------------------ execution */

@@ -18,6 +18,7 @@
 #include "kernels.cuh"
 #include "launch.cuh"
 #include "registry.h"
+#include "tc_kernels.cuh"
 
 extern const ag::EntryTableFn g_entry_tables[];
 extern const int g_num_entry_tables;
@@ -87,7 +88,11 @@ ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
 
 std::string config_str(const ag_config& c) {
     char buf[128];
-    const char* fam = c.family == AG_FAMILY_DIRECT ? "direct" : (c.family == AG_FAMILY_SPLITK ? "splitk" : "indirect");
+    const char* fam = c.family == AG_FAMILY_DIRECT   ? "direct"
+                      : c.family == AG_FAMILY_SPLITK ? "splitk"
+                      : c.family == AG_FAMILY_TF32   ? "tf32"
+                      : c.family == AG_FAMILY_BF16   ? "bf16"
+                                                     : "indirect";
     snprintf(buf, sizeof buf, "%s:%d-%d-%d-%d-%d-%d", fam, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk);
     return buf;
 }
@@ -271,6 +276,14 @@ const char* ag_version(void) { return "adaptgemm-b200 0.1.0 (sm_100a)"; }
 int ag_is_legal(const ag_config* c, const ag_caps* caps) {
     if (!c || !caps) return 0;
     if (std::min({c->bm, c->bn, c->bk, c->tm, c->tn, c->uk}) < 1) return 0;
+    if (c->family == AG_FAMILY_TF32 || c->family == AG_FAMILY_BF16) {
+        // spaces.is_legal_tuple: tensor-core resources are TMEM and the
+        // stage ring, not the CUDA-core register / tile caps
+        const int bk = c->family == AG_FAMILY_TF32 ? 32 : 64;
+        const int64_t smem = (int64_t)c->tm * (128 + c->bn) * 128 + 1024 + 256;
+        return c->bm == 128 && c->bk == bk && c->tn == 1 && c->uk == 1 && c->bn % 32 == 0 && c->bn >= 32 &&
+               c->bn <= 256 && c->tm >= 2 && c->tm <= 8 && smem <= 227 * 1024;
+    }
     if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT && c->family != AG_FAMILY_SPLITK) return 0;
     if (c->family == AG_FAMILY_DIRECT && c->uk != 1) return 0;
     if (c->family == AG_FAMILY_SPLITK) {
@@ -296,6 +309,8 @@ int ag_num_kernels(void) { return registry().count; }
 
 size_t ag_workspace_bytes(const ag_shape* s, const ag_config* c, int dtype) {
     if (!s || !c || c->family == AG_FAMILY_DIRECT || !in_range(*c)) return 0;
+    if (c->family == AG_FAMILY_TF32) return ag::tc::workspace_bytes<ag::tc::KIND_TF32>(s->m, s->n, s->k, c->bn);
+    if (c->family == AG_FAMILY_BF16) return ag::tc::workspace_bytes<ag::tc::KIND_BF16>(s->m, s->n, s->k, c->bn);
     const int splits = c->family == AG_FAMILY_SPLITK ? c->uk : 1;
     if (dtype == AG_F64) return ag::indirect_workspace_bytes<double>(s->m, s->n, s->k, c->bm, c->bn, c->bk, splits);
     return ag::indirect_workspace_bytes<float>(s->m, s->n, s->k, c->bm, c->bn, c->bk, splits);

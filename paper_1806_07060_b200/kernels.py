@@ -36,23 +36,32 @@ class ConfigError(ValueError):
 
 
 class KernelFamily(str, Enum):
-    """The reference's two families plus the B200-profile split-K family.
+    """The reference's two families plus the B200 families.
 
     SPLITK runs the indirect core over `unroll_k` equal K slices and adds
     the slices in a fixed order (deterministic); it exists only in the B200
-    profile, so reference-profile spaces, tables and dispatchers are
-    unchanged.
+    profiles.  TF32 / BF16 are the tensor-core families (tcgen05.mma, TMEM
+    accumulators, TMA): float32 operands packed to tf32 (round to nearest)
+    or bf16, fp32 accumulation; they exist only in the "b200tc" profile.
+    Reference-profile spaces, tables and dispatchers are unchanged.
     """
 
     DIRECT = "direct"
     INDIRECT = "indirect"
     SPLITK = "splitk"
+    TF32 = "tf32"
+    BF16 = "bf16"
+
+
+TC_FAMILIES = (KernelFamily.TF32, KernelFamily.BF16)
 
 
 REFERENCE_FAMILIES = (KernelFamily.DIRECT, KernelFamily.INDIRECT)
 _FAMILY_CODE = {KernelFamily.DIRECT: _native.AG_FAMILY_DIRECT,
                 KernelFamily.INDIRECT: _native.AG_FAMILY_INDIRECT,
-                KernelFamily.SPLITK: _native.AG_FAMILY_SPLITK}
+                KernelFamily.SPLITK: _native.AG_FAMILY_SPLITK,
+                KernelFamily.TF32: _native.AG_FAMILY_TF32,
+                KernelFamily.BF16: _native.AG_FAMILY_BF16}
 _CODE_FAMILY = {v: k for k, v in _FAMILY_CODE.items()}
 
 
@@ -106,13 +115,21 @@ class DeviceCaps:
                      "register_tile_cap_indirect", "element_size", "max_threads"):
             if getattr(self, name) < 1:
                 raise ConfigError(f"{name} must be positive")
-        if self.profile not in (spaces.PROFILE_REFERENCE, spaces.PROFILE_B200):
+        if self.profile not in spaces.PROFILES:
             raise ConfigError(f"unknown caps profile {self.profile!r}")
 
     @classmethod
     def b200(cls, **overrides) -> "DeviceCaps":
         kw = dict(spaces.B200_CAPS)
         kw["profile"] = spaces.PROFILE_B200
+        kw.update(overrides)
+        return cls(**kw)
+
+    @classmethod
+    def b200_tc(cls, **overrides) -> "DeviceCaps":
+        """The B200 profile plus the tensor-core families (tf32, bf16)."""
+        kw = dict(spaces.B200_CAPS)
+        kw["profile"] = spaces.PROFILE_B200_TC
         kw.update(overrides)
         return cls(**kw)
 
@@ -187,6 +204,10 @@ INDIRECT_DOMAINS = spaces.INDIRECT_DOMAINS
 
 
 def domains_for(family: KernelFamily) -> dict[str, tuple[int, ...]]:
+    if family in TC_FAMILIES:
+        return {"block_m": (spaces.TC_BLOCK_M,), "block_n": spaces.TC_BLOCK_N,
+                "block_k": (spaces.TC_BLOCK_K[family.value],), "tile_m": spaces.TC_STAGES,
+                "tile_n": (1,), "unroll_k": (1,)}
     if family is KernelFamily.SPLITK:
         return {"block_m": tuple(sorted({t[0] for t in spaces.SPLITK_TILES})),
                 "block_n": tuple(sorted({t[1] for t in spaces.SPLITK_TILES})),
@@ -215,7 +236,7 @@ def enumerate_search_space(family: KernelFamily, caps: DeviceCaps = DeviceCaps()
 
 def full_search_space(caps: DeviceCaps = DeviceCaps()) -> list[KernelConfig]:
     """All families concatenated: direct block first, then indirect (then, in
-    the B200 profile only, split-K)."""
+    the B200 profiles only, split-K, and in b200tc the tf32/bf16 families)."""
     out = []
     for fam in KernelFamily:
         out.extend(enumerate_search_space(fam, caps))
@@ -331,7 +352,8 @@ def native_shape(shape: ProblemShape) -> _native.AgShape:
 
 def reads_c(shape: ProblemShape, config: KernelConfig) -> bool:
     """Whether the family path reads C: always for direct (kernels.py:227),
-    only when beta != 0 for indirect / split-K (kernels.py:318-321)."""
+    only when beta != 0 for indirect / split-K / tensor-core families
+    (kernels.py:318-321)."""
     return config.family is KernelFamily.DIRECT or shape.beta != 0.0
 
 

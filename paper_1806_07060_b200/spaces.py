@@ -51,10 +51,36 @@ SPLITK_TILES = ((16, 16, 2, 2), (32, 16, 4, 2), (16, 32, 2, 4), (32, 32, 4, 4), 
                 (128, 64, 8, 4), (64, 128, 4, 8), (128, 64, 8, 8), (64, 128, 8, 8), (128, 128, 8, 8))
 SPLITK_BLOCK_K = (16, 32)
 SPLITK_SLICES = (2, 4, 8, 16)
-FAMILIES = ("direct", "indirect", "splitk")
+
+# B200 tensor-core profile ("b200tc"), families "tf32" and "bf16": tcgen05.mma
+# with TMEM accumulators fed by TMA (csrc/tc_kernels.cuh).  bm = 128 is the
+# UMMA M, bn the UMMA N, bk one 128-byte K block (32 tf32 / 64 bf16
+# elements), tm the shared-memory pipeline depth; tn = uk = 1.  They enter
+# only the b200tc search space: their numerics (tf32 / bf16 inputs, fp32
+# accumulation) differ from the fp32 families, so fp32 tables and trees
+# keep their meaning.
+TC_FAMILIES = ("tf32", "bf16")
+TC_BLOCK_M = 128
+TC_BLOCK_N = (64, 128, 256)
+TC_BLOCK_K = {"tf32": 32, "bf16": 64}
+TC_STAGES = (2, 3, 4, 6)
+TC_SMEM_LIMIT = 227 * 1024
+FAMILIES = ("direct", "indirect", "splitk") + TC_FAMILIES
 
 PROFILE_REFERENCE = "reference"
 PROFILE_B200 = "b200"
+PROFILE_B200_TC = "b200tc"
+PROFILES = (PROFILE_REFERENCE, PROFILE_B200, PROFILE_B200_TC)
+
+
+def is_b200_profile(profile) -> bool:
+    """The B200 profiles share the fp32 space; b200tc adds the tc families."""
+    return profile in (PROFILE_B200, PROFILE_B200_TC)
+
+
+def tc_smem_bytes(bn, stages) -> int:
+    """Dynamic shared memory of one tc CTA: the stage ring + slack + barriers."""
+    return stages * (TC_BLOCK_M + bn) * 128 + 1024 + 256
 
 # DeviceCaps defaults (kernels.py:64-71) and the B200 profile caps
 REFERENCE_CAPS = dict(tile_memory_cap=32768, register_tile_cap_direct=8,
@@ -80,6 +106,12 @@ def is_legal_tuple(family, bm, bn, bk, tm, tn, uk, caps) -> bool:
         return False
     if family not in FAMILIES:
         return False
+    if family in TC_FAMILIES:
+        # tensor-core resources are TMEM and the stage ring, not the
+        # CUDA-core register/tile caps
+        return (bm == TC_BLOCK_M and bk == TC_BLOCK_K[family] and tn == 1 and uk == 1
+                and bn % 32 == 0 and 32 <= bn <= 256 and 2 <= tm <= 8
+                and tc_smem_bytes(bn, tm) <= TC_SMEM_LIMIT)
     if family == "direct" and uk != 1:
         return False
     if family == "splitk":
@@ -109,14 +141,19 @@ def _product(family, domains):
 
 def enumerate_tuples(family, caps, profile=PROFILE_REFERENCE):
     """Legal configs of one family in deterministic canonical order."""
+    if family in TC_FAMILIES:
+        if profile != PROFILE_B200_TC:
+            return []
+        return [t for bn in TC_BLOCK_N for st in TC_STAGES
+                for t in [(family, TC_BLOCK_M, bn, TC_BLOCK_K[family], st, 1, 1)] if is_legal_tuple(*t, caps)]
     if family == "splitk":
-        if profile != PROFILE_B200:
+        if not is_b200_profile(profile):
             return []
         return [t for (bm, bn, tm, tn) in SPLITK_TILES for bk in SPLITK_BLOCK_K for s in SPLITK_SLICES
                 for t in [("splitk", bm, bn, bk, tm, tn, s)] if is_legal_tuple(*t, caps)]
     base = DIRECT_DOMAINS if family == "direct" else INDIRECT_DOMAINS
     out = [t for t in _product(family, base) if is_legal_tuple(*t, caps)]
-    if profile == PROFILE_B200 and family == "indirect":
+    if is_b200_profile(profile) and family == "indirect":
         seen = set(out)
         for t in _product(family, B200_INDIRECT_EXTRA_DOMAINS):
             bm, bn = t[1], t[2]

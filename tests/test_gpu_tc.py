@@ -1,0 +1,121 @@
+"""GPU parity of the tensor-core families (tf32, bf16; csrc/tc_kernels.cuh).
+
+No reference analogue (BASELINE.json configs[4] adds them to the search
+space).  Bars, as SURVEY.md section 8(c) states them:
+* vs the float64 reference on the float32 inputs: relative Frobenius error
+  <= 1e-3 (tf32) / <= 1e-2 (bf16) -- the input-rounding floor is ~2.6e-4 /
+  ~2.1e-3 independent of K;
+* vs the float64 reference on inputs pre-rounded the way the pack rounds
+  them (tf32: round to nearest, ties away; bf16: round to nearest even):
+  <= 1e-5, i.e. only fp32 accumulation error remains.
+beta == 0 never reads C (the indirect family's semantics, kernels.py:318-321).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import rand_operands, rel_frobenius
+from oracle import gemm as ogemm
+from paper_1806_07060_b200.kernels import (DeviceCaps, KernelConfig, KernelFamily, ProblemShape,
+                                           enumerate_search_space, gemm_execute)
+
+pytestmark = pytest.mark.gpu
+
+TC = DeviceCaps.b200_tc()
+RF_TOL = {KernelFamily.TF32: 1e-3, KernelFamily.BF16: 1e-2}
+RF_TOL_ROUNDED = 1e-5
+
+
+def round_tf32(x):
+    """cvt.rna.tf32.f32: keep 10 mantissa bits, round half away from zero."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32)
+    return ((b + np.uint32(0x1000)) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+def round_bf16(x):
+    """__float2bfloat16_rn: keep 7 mantissa bits, round half to even."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return r.astype(np.uint32).view(np.float32)
+
+
+ROUND = {KernelFamily.TF32: round_tf32, KernelFamily.BF16: round_bf16}
+
+
+def _ref(s, A, B, C):
+    return ogemm.reference(s.M, s.N, s.K, s.alpha, s.beta, s.transA, s.transB, A, B, C)
+
+
+def _check(s, cfg, seed=0):
+    A, B, C = rand_operands(s, np.float32, seed)
+    out, sec = gemm_execute(s, cfg, A, B, C, TC)
+    assert sec > 0
+    err = rel_frobenius(out, _ref(s, A, B, C))
+    assert err <= RF_TOL[cfg.family], (cfg.canonical(), s, err)
+    rnd = ROUND[cfg.family]
+    err_r = rel_frobenius(out, _ref(s, rnd(A), rnd(B), C))
+    assert err_r <= RF_TOL_ROUNDED, (cfg.canonical(), s, err_r)
+    return err, err_r
+
+
+def _configs(fam):
+    return enumerate_search_space(fam, TC)
+
+
+def test_tc_space_enumerates_only_in_tc_profile():
+    for fam in (KernelFamily.TF32, KernelFamily.BF16):
+        assert enumerate_search_space(fam, DeviceCaps.b200()) == []
+        assert len(_configs(fam)) >= 6
+
+
+@pytest.mark.parametrize("fam", [KernelFamily.TF32, KernelFamily.BF16], ids=lambda f: f.value)
+@pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 13, 5), (128, 128, 32), (129, 257, 33), (35, 1000, 2560),
+                                 (300, 64, 1), (64, 300, 4097)])
+@pytest.mark.parametrize("trans", [(False, False), (True, False), (False, True), (True, True)],
+                         ids=["NN", "TN", "NT", "TT"])
+def test_tc_shapes_and_transposes(fam, mnk, trans):
+    s = ProblemShape(*mnk, alpha=1.0, beta=0.0, transA=trans[0], transB=trans[1])
+    _check(s, _configs(fam)[0])
+
+
+@pytest.mark.parametrize("fam", [KernelFamily.TF32, KernelFamily.BF16], ids=lambda f: f.value)
+def test_tc_every_config(fam):
+    # 333 x 517 x 260: ragged in every dimension; the persistent grid wraps
+    # when tiles exceed the SM count (checked at 2048^2 below)
+    s = ProblemShape(333, 517, 260, alpha=1.25, beta=-0.5)
+    for cfg in _configs(fam):
+        _check(s, cfg)
+
+
+@pytest.mark.parametrize("fam", [KernelFamily.TF32, KernelFamily.BF16], ids=lambda f: f.value)
+def test_tc_persistent_wrap_rows(fam):
+    """2048 x 2048 x 1024: up to 512 tiles over 148 persistent CTAs.  Checked
+    on 64 exact rows spread over the matrix (pre-rounded float64)."""
+    s = ProblemShape(2048, 2048, 1024)
+    A, B, C = rand_operands(s, np.float32, 3)
+    rnd = ROUND[fam]
+    rows = np.arange(0, 2048, 32)
+    exact = rnd(A)[rows].astype(np.float64) @ rnd(B).astype(np.float64)
+    for cfg in _configs(fam):
+        out, _ = gemm_execute(s, cfg, A, B, C, TC)
+        assert rel_frobenius(out[rows], exact) <= RF_TOL_ROUNDED, cfg.canonical()
+
+
+@pytest.mark.parametrize("fam", [KernelFamily.TF32, KernelFamily.BF16], ids=lambda f: f.value)
+def test_tc_beta_zero_never_reads_c(fam):
+    s = ProblemShape(70, 90, 40, alpha=2.0, beta=0.0)
+    A, B, C = rand_operands(s, np.float32, 5)
+    C[:] = np.nan
+    out, _ = gemm_execute(s, _configs(fam)[0], A, B, C, TC)
+    assert np.isfinite(out).all()
+    s1 = ProblemShape(70, 90, 40, alpha=2.0, beta=1.0)
+    out1, _ = gemm_execute(s1, _configs(fam)[0], A, B, C, TC)
+    assert np.isnan(out1).all()
+
+
+def test_tc_rejects_float64():
+    from paper_1806_07060_b200.kernels import ConfigError
+    s = ProblemShape(16, 16, 16)
+    A, B, C = rand_operands(s, np.float64)
+    with pytest.raises(ConfigError):
+        gemm_execute(s, _configs(KernelFamily.TF32)[0], A, B, C, TC)
