@@ -309,8 +309,8 @@ int ag_num_kernels(void) { return registry().count; }
 
 size_t ag_workspace_bytes(const ag_shape* s, const ag_config* c, int dtype) {
     if (!s || !c || c->family == AG_FAMILY_DIRECT || !in_range(*c)) return 0;
-    if (c->family == AG_FAMILY_TF32) return ag::tc::workspace_bytes<ag::tc::KIND_TF32>(s->m, s->n, s->k, c->bn);
-    if (c->family == AG_FAMILY_BF16) return ag::tc::workspace_bytes<ag::tc::KIND_BF16>(s->m, s->n, s->k, c->bn);
+    if (c->family == AG_FAMILY_TF32) return ag::tc::workspace_bytes<ag::tc::KIND_TF32>(s->m, s->n, s->k, s->trans_a, s->trans_b);
+    if (c->family == AG_FAMILY_BF16) return ag::tc::workspace_bytes<ag::tc::KIND_BF16>(s->m, s->n, s->k, s->trans_a, s->trans_b);
     const int splits = c->family == AG_FAMILY_SPLITK ? c->uk : 1;
     if (dtype == AG_F64) return ag::indirect_workspace_bytes<double>(s->m, s->n, s->k, c->bm, c->bn, c->bk, splits);
     return ag::indirect_workspace_bytes<float>(s->m, s->n, s->k, c->bm, c->bn, c->bk, splits);

@@ -2,13 +2,17 @@
 //
 // No reference analogue: the reference's two families are CUDA-core style
 // loop nests (kernels.py:198-260).  These families serve the dense
-// contraction on the 5th-generation tensor cores (BASELINE.json configs[4])
-// and follow the indirect family's structure (kernels.py:304-325): an O(n^2)
-// helper pass packs op(A) and op(B)^T into zero-padded, K-major buffers in
-// the MMA element type (tf32 = fp32 rounded to nearest, bf16 = round to
-// nearest even), then an unpredicated core runs on exact tile multiples and
-// a masked epilogue writes alpha * acc + beta * C (C read only when
-// beta != 0, as the indirect family, kernels.py:318-321).
+// contraction on the 5th-generation tensor cores (BASELINE.json configs[4]).
+// Operands are read where they lie, in either major: op(A) is K-major
+// (MN-major when transA), op(B) is MN-major (K-major when transB); the
+// tensor core takes both, so nothing is transposed or padded -- the TMA unit
+// zero-fills boxes that run past M, N or K.  tf32 reads the caller's fp32
+// matrices in place (the tensor core consumes the fp32 bits as tf32); bf16
+// needs one streaming convert pass per operand (fp32 -> bf16, round to
+// nearest even, layout kept), the helper pass of this family as the packs
+// are the indirect family's (kernels.py:304-325).  The epilogue writes
+// alpha * acc + beta * C, reading C only when beta != 0 (the indirect
+// family's semantics, kernels.py:318-321).
 //
 // Core (tc_gemm_kernel): persistent, warp specialised, one CTA per SM.
 //   warp 0 lane 0 : TMA producer -- cp.async.bulk.tensor 2D loads of the
@@ -98,19 +102,31 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-// K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100 format):
-// start address, LBO (unused for swizzled K-major), SBO = 1024 B between
-// 8-row groups, version 1, layout type 2 (128B swizzle).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+// SWIZZLE_128B shared-memory matrix descriptors (sm_100 format: start
+// address >> 4, LBO >> 4 at bit 16, SBO >> 4 at bit 32, version 1 at bit
+// 46, layout type 2 = 128-byte swizzle at bit 61).
+//  K-major  (a row of the tile = 128 bytes of K): SBO = 1024 B between
+//           8-row groups; LBO unused.  One UMMA_K step = +32 bytes.
+//  MN-major (a row of the tile = 128 bytes of M or N, one row per k):
+//           SBO = 1024 B between 8-k groups, LBO = distance between the
+//           128-byte MN chunks (BK * 128 B: each chunk is one TMA box of
+//           BK rows).  One UMMA_K step = +UMMA_K * 128 bytes.
+//           32-bit (tf32) MN-major operands use the 128-byte swizzle with
+//           32-byte atoms instead (layout type 1, "128B_BASE32B": 32-byte
+//           chunks XORed by k % 4, written by the TMA's SWIZZLE_128B_ATOM_32B
+//           mode), so SBO = 512 B between 4-k groups.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_bytes = 16, uint32_t sbo_bytes = 1024,
+                                               uint32_t layout = 2) {
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo_bytes >> 4) << 16) |
+           ((uint64_t)(sbo_bytes >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
 }
 
-// instruction descriptor: D f32, A/B format, both K-major, N >> 3, M >> 4
-template <int KIND, int N>
-__host__ __device__ constexpr uint32_t instr_desc() {
-    return (1u << 4) | (Elem<KIND>::FMT << 7) | (Elem<KIND>::FMT << 10) | ((uint32_t)(N >> 3) << 17) |
-           ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor: D f32, A/B format, A/B major (0 = K, 1 = MN),
+// N >> 3, M >> 4
+template <int KIND>
+__host__ __device__ constexpr uint32_t instr_desc(int n, int a_mn, int b_mn) {
+    return (1u << 4) | (Elem<KIND>::FMT << 7) | (Elem<KIND>::FMT << 10) | ((uint32_t)a_mn << 15) |
+           ((uint32_t)b_mn << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 template <int KIND>
@@ -147,6 +163,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 struct TcParams {
     int M, N, tiles_m, tiles_n, k_blocks, group_m;
+    int a_mn, b_mn;   // operand majors: 0 = K-major, 1 = MN-major
+    uint32_t idesc;
     float alpha, beta;
     int use_c, vec_out;
     const float* C;
@@ -183,8 +201,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     constexpr uint32_t A_BYTES = BM * ROW_BYTES, B_BYTES = BN * ROW_BYTES;
     constexpr uint32_t STAGE_TX = A_BYTES + B_BYTES;
     constexpr uint32_t TMEM_COLS = tmem_cols<BN>();
-    constexpr uint32_t IDESC = instr_desc<KIND, BN>();
     constexpr int K_STEPS = BK / Elem<KIND>::UMMA_K;
+    constexpr int CH = ROW_BYTES / (int)sizeof(typename Elem<KIND>::T);  // elements per 128-byte MN chunk
+    constexpr uint32_t CHUNK_BYTES = BK * ROW_BYTES;                      // one MN chunk of one stage
+    constexpr uint32_t MN_SBO = KIND == KIND_TF32 ? 512 : 1024;           // see sw128_desc
+    constexpr uint32_t MN_LAYOUT = KIND == KIND_TF32 ? 1 : 2;
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 is 16..256 in steps of 16");
     static_assert(BN % 32 == 0, "epilogue drains 32 columns per tcgen05.ld");
 
@@ -234,8 +255,22 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], STAGE_TX);
-                    tma_load_2d(sA + stage * A_BYTES, &mapA, &full[stage], kb * BK, tm * BM);
-                    tma_load_2d(sB + stage * B_BYTES, &mapB, &full[stage], kb * BK, tn * BN);
+                    uint8_t* a = sA + stage * A_BYTES;
+                    uint8_t* b = sB + stage * B_BYTES;
+                    if (!p.a_mn) {
+                        tma_load_2d(a, &mapA, &full[stage], kb * BK, tm * BM);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < BM / CH; ++c)
+                            tma_load_2d(a + c * CHUNK_BYTES, &mapA, &full[stage], tm * BM + c * CH, kb * BK);
+                    }
+                    if (!p.b_mn) {
+                        tma_load_2d(b, &mapB, &full[stage], kb * BK, tn * BN);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < BN / CH; ++c)
+                            tma_load_2d(b + c * CHUNK_BYTES, &mapB, &full[stage], tn * BN + c * CH, kb * BK);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -256,8 +291,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                     tc_fence_after();
                     const uint32_t a0 = smem_addr(sA + stage * A_BYTES), b0 = smem_addr(sB + stage * B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < K_STEPS; ++k)
-                        umma<KIND>(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), IDESC, (kb | k) != 0);
+                    for (int k = 0; k < K_STEPS; ++k) {
+                        const uint64_t ad =
+                            p.a_mn ? sw128_desc(a0 + k * Elem<KIND>::UMMA_K * ROW_BYTES, CHUNK_BYTES, MN_SBO, MN_LAYOUT)
+                                   : sw128_desc(a0 + k * 32);
+                        const uint64_t bd =
+                            p.b_mn ? sw128_desc(b0 + k * Elem<KIND>::UMMA_K * ROW_BYTES, CHUNK_BYTES, MN_SBO, MN_LAYOUT)
+                                   : sw128_desc(b0 + k * 32);
+                        umma<KIND>(d, ad, bd, p.idesc, (kb | k) != 0);
+                    }
                     umma_commit(&empty[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
@@ -337,43 +379,54 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     }
 }
 
-// helper pass: dst (dst_rows x dst_cols, ld_dst) = zero-padded op(src)
-// converted to the MMA element type; op = transpose when `transpose`
-// (src then holds the cols x rows matrix).  32x32 tile through smem so
-// both sides are coalesced.
-__device__ __forceinline__ float to_elem(float x, float*) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+// helper pass (bf16 always; tf32 only when an operand's rows are not
+// 16-byte aligned): dst (rows x cols, ld_dst) = src converted to the MMA
+// element type, layout unchanged (no transpose: the core reads either
+// major).  bf16 rounds to nearest even; the tf32 copy keeps the fp32 bits
+// (the tensor core consumes them as tf32).  Four elements per thread,
+// 16-byte loads when the source rows allow it.
+__device__ __forceinline__ void store4(float* d, float a, float b, float c, float e, bool vec) {
+    if (vec) {
+        *reinterpret_cast<float4*>(d) = make_float4(a, b, c, e);
+    } else {
+        d[0] = a; d[1] = b; d[2] = c; d[3] = e;
+    }
 }
-__device__ __forceinline__ __nv_bfloat16 to_elem(float x, __nv_bfloat16*) { return __float2bfloat16_rn(x); }
+__device__ __forceinline__ void store4(__nv_bfloat16* d, float a, float b, float c, float e, bool vec) {
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, e);
+    if (vec) {
+        uint2 u;
+        u.x = *reinterpret_cast<const uint32_t*>(&lo);
+        u.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(d) = u;
+    } else {
+        d[0] = lo.x; d[1] = lo.y; d[2] = hi.x; d[3] = hi.y;
+    }
+}
+__device__ __forceinline__ void store1(float* d, float a) { *d = a; }
+__device__ __forceinline__ void store1(__nv_bfloat16* d, float a) { *d = __float2bfloat16_rn(a); }
 
 template <typename D>
 __global__ void __launch_bounds__(256)
-tc_pack_kernel(D* __restrict__ dst, i64 ld_dst, int dst_rows, int dst_cols, const float* __restrict__ src,
-               i64 ld_src, int rows, int cols, int transpose) {
-    __shared__ float tile[32][33];
-    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-    const int x = threadIdx.x, y = threadIdx.y;
-    if (transpose) {
-#pragma unroll
-        for (int yy = y; yy < 32; yy += 8) {
-            const int c = c0 + yy, r = r0 + x;
-            tile[yy][x] = (r < rows && c < cols) ? src[(i64)c * ld_src + r] : 0.0f;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int yy = y; yy < 32; yy += 8) {
-            const int r = r0 + yy, c = c0 + x;
-            if (r < dst_rows && c < dst_cols) dst[(i64)r * ld_dst + c] = to_elem(tile[x][yy], (D*)nullptr);
-        }
-    } else {
-#pragma unroll
-        for (int yy = y; yy < 32; yy += 8) {
-            const int r = r0 + yy, c = c0 + x;
-            if (r < dst_rows && c < dst_cols)
-                dst[(i64)r * ld_dst + c] =
-                    to_elem((r < rows && c < cols) ? src[(i64)r * ld_src + c] : 0.0f, (D*)nullptr);
+tc_convert_kernel(D* __restrict__ dst, i64 ld_dst, const float* __restrict__ src, i64 ld_src, int rows, int cols,
+                  int src_vec) {
+    const int quads = (cols + 3) >> 2;
+    for (int r = blockIdx.y; r < rows; r += gridDim.y) {
+        const float* s = src + (i64)r * ld_src;
+        D* d = dst + (i64)r * ld_dst;
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
+            const int c = q << 2;
+            if (c + 4 <= cols) {
+                float4 v;
+                if (src_vec) {
+                    v = __ldcs(reinterpret_cast<const float4*>(s + c));
+                } else {
+                    v = make_float4(s[c], s[c + 1], s[c + 2], s[c + 3]);
+                }
+                store4(d + c, v.x, v.y, v.z, v.w, true);
+            } else {
+                for (int j = c; j < cols; ++j) store1(d + j, s[j]);
+            }
         }
     }
 }
@@ -403,37 +456,63 @@ inline int sm_count() {
     return n;
 }
 
-// K-major (rows x cols) matrix with leading dimension `cols`, 128-byte boxes
+// One operand as stored: `rows` x `cols` row-major with leading dimension
+// `ld` (elements of the MMA type).  K-major when the contiguous dimension is
+// K (box: 128 bytes of K x `box_rows` rows), MN-major when it is M or N
+// (box: 128 bytes of MN x BK rows of k; the producer issues one box per
+// 128-byte chunk).  Out-of-range boxes are zero-filled by the TMA unit, so
+// no operand is padded to the tile.
 template <int KIND>
-inline bool make_map(CUtensorMap* map, const void* base, i64 rows, i64 cols, int box_rows) {
+inline bool make_map(CUtensorMap* map, const void* base, i64 rows, i64 cols, i64 ld, bool mn_major, int box_rows) {
     auto fn = encode_fn();
     if (!fn) return false;
     typedef typename Elem<KIND>::T T;
+    constexpr int CH = ROW_BYTES / (int)sizeof(T);
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(cols * (i64)sizeof(T))};
-    cuuint32_t box[2] = {(cuuint32_t)Elem<KIND>::BK, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * (i64)sizeof(T))};
+    cuuint32_t box[2] = {(cuuint32_t)CH, (cuuint32_t)(mn_major ? Elem<KIND>::BK : box_rows)};
     cuuint32_t estr[2] = {1, 1};
+    // 32-bit MN-major tiles: 32-byte swizzle atoms (see sw128_desc)
+    const CUtensorMapSwizzle swz =
+        (KIND == KIND_TF32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
     CUresult r = fn(map, Elem<KIND>::TMA, 2, const_cast<void*>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-// [Ap (Mp x Kp) | Bp (Np x Kp)] in the element type, each 1024-byte aligned
+// stored (rows, cols) of op(A) and op(B): A is M x K (K x M when transA),
+// B is K x N (N x K when transB)
+struct OperandLayout {
+    i64 rows, cols;
+};
+inline OperandLayout layout_a(i64 M, i64 K, int ta) { return ta ? OperandLayout{K, M} : OperandLayout{M, K}; }
+inline OperandLayout layout_b(i64 N, i64 K, int tb) { return tb ? OperandLayout{N, K} : OperandLayout{K, N}; }
+
 template <int KIND>
-inline size_t workspace_bytes(i64 M, i64 N, i64 K, int bn) {
+inline i64 staged_ld(i64 cols) {
+    return round_up_i(cols, 16 / (i64)sizeof(typename Elem<KIND>::T));
+}
+
+// [A staging | B staging], each 1024-byte aligned: converted (bf16) or
+// re-strided (tf32, only used when a row stride is not 16-byte aligned)
+template <int KIND>
+inline size_t workspace_bytes(i64 M, i64 N, i64 K, int ta, int tb) {
     typedef typename Elem<KIND>::T T;
-    const i64 Mp = round_up_i(M, BM), Np = round_up_i(N, bn), Kp = round_up_i(K, Elem<KIND>::BK);
-    return (size_t)round_up_i(Mp * Kp * (i64)sizeof(T), 1024) + (size_t)round_up_i(Np * Kp * (i64)sizeof(T), 1024);
+    const OperandLayout a = layout_a(M, K, ta), b = layout_b(N, K, tb);
+    return (size_t)round_up_i(a.rows * staged_ld<KIND>(a.cols) * (i64)sizeof(T), 1024) +
+           (size_t)round_up_i(b.rows * staged_ld<KIND>(b.cols) * (i64)sizeof(T), 1024);
 }
 
 template <int KIND>
-inline int launch_pack(typename Elem<KIND>::T* dst, i64 dst_rows, i64 dst_cols, const float* src, i64 ld_src,
-                       i64 rows, i64 cols, int transpose, cudaStream_t stream) {
-    dim3 grid((unsigned)((dst_cols + 31) / 32), (unsigned)((dst_rows + 31) / 32));
-    if (grid.y > 65535u) return AG_ERR_SHAPE;
-    tc_pack_kernel<typename Elem<KIND>::T><<<grid, dim3(32, 8), 0, stream>>>(
-        dst, dst_cols, (int)dst_rows, (int)dst_cols, src, ld_src, (int)rows, (int)cols, transpose);
+inline int launch_convert(typename Elem<KIND>::T* dst, i64 ld_dst, const float* src, i64 ld_src, i64 rows, i64 cols,
+                          cudaStream_t stream) {
+    const int src_vec = (ld_src % 4 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+    const i64 quads = (cols + 3) / 4;
+    const unsigned gx = (unsigned)std::min<i64>((quads + 255) / 256, 64);
+    const unsigned gy = (unsigned)std::min<i64>(rows, 65535);
+    tc_convert_kernel<typename Elem<KIND>::T><<<dim3(gx, gy), 256, 0, stream>>>(dst, ld_dst, src, ld_src, (int)rows,
+                                                                                 (int)cols, src_vec);
     return cudaGetLastError() == cudaSuccess ? AG_OK : AG_ERR_CUDA;
 }
 
@@ -442,37 +521,63 @@ inline int tc_fail(const GemmCall& c, int code, const char* msg) {
     return code;
 }
 
+// Stage one operand for the TMA: bf16 always converts into the workspace;
+// tf32 reads the caller's fp32 matrix in place when its base and row stride
+// are 16-byte aligned, else copies it to a re-strided buffer.
+template <int KIND>
+inline int stage_operand(const float* src, i64 ld_src, OperandLayout lay, void* ws, const void** base, i64* ld,
+                         cudaStream_t stream) {
+    typedef typename Elem<KIND>::T T;
+    if (KIND == KIND_TF32 && ld_src % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+        *base = src;
+        *ld = ld_src;
+        return AG_OK;
+    }
+    *ld = staged_ld<KIND>(lay.cols);
+    *base = ws;
+    return launch_convert<KIND>(static_cast<T*>(ws), *ld, src, ld_src, lay.rows, lay.cols, stream);
+}
+
 template <int KIND, int BN, int STAGES>
 int launch_tc(const GemmCall& c) {
     typedef typename Elem<KIND>::T T;
     constexpr int BK = Elem<KIND>::BK;
     if (c.dtype != AG_F32) return tc_fail(c, AG_ERR_CONFIG, "tensor-core families take float32 operands");
     const i64 M = c.M, N = c.N, K = c.K;
-    const i64 Mp = round_up_i(M, BM), Np = round_up_i(N, BN), Kp = round_up_i(K, BK);
-    if (Mp > 0x7fffffffLL || Np > 0x7fffffffLL || Kp > 0x7fffffffLL)
-        return tc_fail(c, AG_ERR_SHAPE, "dimension too large");
-    const size_t need = workspace_bytes<KIND>(M, N, K, BN);
-    if (c.ws_bytes < need || c.ws == nullptr)
-        return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core pack buffers");
-    T* Ap = static_cast<T*>(c.ws);
-    T* Bp = reinterpret_cast<T*>(static_cast<char*>(c.ws) + round_up_i(Mp * Kp * (i64)sizeof(T), 1024));
-    // op(A) -> Ap[m][k]; op(B)^T -> Bp[n][k]
-    int r = launch_pack<KIND>(Ap, Mp, Kp, static_cast<const float*>(c.A), c.lda, M, K, c.ta ? 1 : 0, c.stream);
-    if (r) return tc_fail(c, r, "pack of op(A) failed");
-    r = launch_pack<KIND>(Bp, Np, Kp, static_cast<const float*>(c.B), c.ldb, N, K, c.tb ? 0 : 1, c.stream);
-    if (r) return tc_fail(c, r, "pack of op(B) failed");
+    const i64 tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN, k_blocks = (K + BK - 1) / BK;
+    if (tiles_m * tiles_n > 0x7fffffffLL || k_blocks > 0x7fffffffLL)
+        return tc_fail(c, AG_ERR_SHAPE, "problem too large for the tensor-core grid");
+    const OperandLayout la = layout_a(M, K, c.ta), lb = layout_b(N, K, c.tb);
+    const size_t need = workspace_bytes<KIND>(M, N, K, c.ta, c.tb);
+    if (KIND == KIND_BF16 && (c.ws_bytes < need || c.ws == nullptr))
+        return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
+    char* wsA = static_cast<char*>(c.ws);
+    char* wsB = wsA ? wsA + round_up_i(la.rows * staged_ld<KIND>(la.cols) * (i64)sizeof(T), 1024) : nullptr;
+    const void *baseA = nullptr, *baseB = nullptr;
+    i64 ldA = 0, ldB = 0;
+    int r = stage_operand<KIND>(static_cast<const float*>(c.A), c.lda, la, wsA, &baseA, &ldA, c.stream);
+    if (r == AG_OK) r = stage_operand<KIND>(static_cast<const float*>(c.B), c.ldb, lb, wsB, &baseB, &ldB, c.stream);
+    if (r) return tc_fail(c, r, "staging of an operand failed");
+    if ((baseA == (const void*)wsA || baseB == (const void*)wsB) && (c.ws_bytes < need || c.ws == nullptr))
+        return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
 
+    // A: K-major unless transA; B: MN-major unless transB
+    const int a_mn = c.ta ? 1 : 0, b_mn = c.tb ? 0 : 1;
     CUtensorMap mapA, mapB;
-    if (!make_map<KIND>(&mapA, Ap, Mp, Kp, BM) || !make_map<KIND>(&mapB, Bp, Np, Kp, BN))
+    if (!make_map<KIND>(&mapA, baseA, la.rows, la.cols, ldA, a_mn, BM) ||
+        !make_map<KIND>(&mapB, baseB, lb.rows, lb.cols, ldB, b_mn, BN))
         return tc_fail(c, AG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 
     TcParams p;
     p.M = (int)M;
     p.N = (int)N;
-    p.tiles_m = (int)(Mp / BM);
-    p.tiles_n = (int)(Np / BN);
-    p.k_blocks = (int)(Kp / BK);
+    p.tiles_m = (int)tiles_m;
+    p.tiles_n = (int)tiles_n;
+    p.k_blocks = (int)k_blocks;
     p.group_m = p.tiles_m < 8 ? p.tiles_m : 8;
+    p.a_mn = a_mn;
+    p.b_mn = b_mn;
+    p.idesc = instr_desc<KIND>(BN, a_mn, b_mn);
     p.alpha = (float)c.alpha;
     p.beta = (float)c.beta;
     p.use_c = c.beta != 0.0;
@@ -482,8 +587,6 @@ int launch_tc(const GemmCall& c) {
     p.ldo = c.ldo;
     p.vec_out = (c.ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(c.out) % 16 == 0) &&
                 (!p.use_c || ((c.ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(c.C) % 16 == 0)));
-    const i64 tiles = (i64)p.tiles_m * p.tiles_n;
-    if (tiles > 0x7fffffffLL) return tc_fail(c, AG_ERR_SHAPE, "too many tiles");
 
     // >= 116 KB of shared memory keeps one CTA per SM, so a CTA never waits
     // on another CTA's TMEM allocation
@@ -496,7 +599,7 @@ int launch_tc(const GemmCall& c) {
             return tc_fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
         attr_done.store(1);
     }
-    const unsigned grid = (unsigned)std::min<i64>(tiles, sm_count());
+    const unsigned grid = (unsigned)std::min<i64>(tiles_m * tiles_n, sm_count());
     kernel<<<grid, THREADS, smem, c.stream>>>(mapA, mapB, p);
     return cudaGetLastError() == cudaSuccess ? AG_OK : tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
 }
