@@ -44,6 +44,7 @@ import numpy as np  # noqa: E402
 DATA = ROOT / "paper_1806_07060_b200" / "data"
 PO2_BUNDLE = DATA / "tables_b200_po2.csv.gz"
 DB_BUNDLE = DATA / "tables_b200_deepbench.csv.gz"
+TC_BUNDLE = DATA / "tables_b200tc_random.csv.gz"
 TRAFFIC_FILE = ROOT / "profiles" / "roofline_traffic.json"
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -114,6 +115,48 @@ def build_model():
     }
 
 
+def build_tc_model(policy):
+    """configs[4]: the reference pipeline on the b200tc tables (random
+    (M, N, K) in 1..8192, tf32/bf16 families + the fp32 winner shortlist;
+    configs/random_tc_b200.json).  Default tile = the fp32 BaselinePolicy of
+    the main model (the reference's definition); `fixed_tc` = the single tc
+    config with the best geomean over the training shapes."""
+    from paper_1806_07060_b200 import evaluation, model
+    from paper_1806_07060_b200.dataset import dataset_from_tables, split
+    from paper_1806_07060_b200.kernels import TC_FAMILIES
+    from paper_1806_07060_b200.tuner import load_table_bundle
+
+    if not TC_BUNDLE.exists():
+        return None
+    tables = load_table_bundle(TC_BUNDLE)
+    ds = dataset_from_tables(tables, "random")
+    sp = split(ds, SPLIT_FRACTION, SPLIT_SEED)
+    recs = ds.features_and_labels()
+    train_recs = [recs[i] for i in sp.train]
+    test_recs = [recs[i] for i in sp.test]
+    named = model.grid_train(train_recs)
+    policy.register(ds.class_index)
+    by_shape = evaluation.tables_by_shape(tables)
+    scores = evaluation.score_models(named, test_recs, by_shape, ds.class_index, policy)
+    best = evaluation.select_best_model(scores)
+    train_shapes = [recs[i][0] for i in sp.train]
+    tc_cfgs = [m.config for m in tables[0].measurements if m.config.family in TC_FAMILIES]
+
+    def train_geo(cfg):
+        return geomean(by_shape[mnk].gflops_for(cfg) for mnk in train_shapes)
+
+    fixed = max(tc_cfgs, key=train_geo)
+    return {"tree": dict(named)[best.name], "name": best.name, "classes": ds.class_index, "tables": by_shape,
+            "test": [ProblemShapeOf(recs[i][0]) for i in sp.test], "fixed_tc": fixed, "n_train": len(train_recs),
+            "score": {"accuracy": best.accuracy, "dtpr": best.dtpr, "dttr": best.dttr,
+                      "leaves": best.stats.total_leaves, "height": best.stats.height}}
+
+
+def ProblemShapeOf(mnk):
+    from paper_1806_07060_b200.kernels import ProblemShape
+    return ProblemShape(*mnk)
+
+
 # ---------------------------------------------------------------------------
 # device-side measurement
 
@@ -121,7 +164,7 @@ def build_model():
 class ShapeCase:
     """Resident operands + prepared native arguments for one shape."""
 
-    def __init__(self, shape, device, seed=0):
+    def __init__(self, shape, device, seed=0, keep_host=True):
         import ctypes
 
         import torch
@@ -133,7 +176,7 @@ class ShapeCase:
         self.shape = shape
         self.flops = 2.0 * shape.M * shape.N * shape.K
         A, B, C, _ = _bench_buffers(shape, np.float32, seed)
-        self.host = (A, B, C)
+        self.host = (A, B, C) if keep_host else None
         self.dA, self.dB, self.dC = (torch.from_numpy(x).to(device) for x in (A, B, C))
         self.dout = torch.empty((shape.M, shape.N), device=device)
         self.nshape = native_shape(shape)
@@ -146,9 +189,11 @@ class ShapeCase:
 
 def pack_launches(shape, cfg) -> int:
     """Kernels one family path launches (mirrors launch.cuh's pack decisions)."""
-    from paper_1806_07060_b200.kernels import KernelFamily
+    from paper_1806_07060_b200.kernels import TC_FAMILIES, KernelFamily
     if cfg.family is KernelFamily.DIRECT:
         return 1
+    if cfg.family in TC_FAMILIES:  # bf16: one convert pass per operand; tf32 reads fp32 in place
+        return 3 if cfg.family is KernelFamily.BF16 else 1
     n = 1
     if not (shape.transA and shape.M % cfg.block_m == 0 and shape.K % cfg.block_k == 0):
         n += 1
@@ -422,6 +467,11 @@ def run_ours(args):
     po2_or = measured(po2_cases, [tables[c.shape.mnk].best_config for c in po2_cases])
     po2_de = measured(po2_cases, [policy.select_config(c.shape) for c in po2_cases])
 
+    # ---- configs[4]: the tensor-core search space on random (M, N, K)
+    tc_doc = tc_section(m, policy, device, distributed, times, fallback, args)
+    # ---- configs[3]: sharded exhaustive sweep throughput
+    sweep_doc = sweep_section(device, distributed, rank, world) if not args.no_sweep else None
+
     # ---- e2e: the public API with host buffers, copies inside the timed call
     from paper_1806_07060_b200.kernels import reads_c
     e2e_t = []
@@ -513,6 +563,8 @@ def run_ours(args):
                      "frac_of_nominal": round(achieved / NOMINAL_FP32_TFLOPS, 4),
                      "note": "event time covers the whole family path (pack helpers + tiled core)"},
         "cpu_baseline": cpu,
+        "tc_random": tc_doc,
+        "sweep": sweep_doc,
         "clocks": clocks,
         "gpu_launches": launches,
         "parity_spot_check_rf": rf,
@@ -523,6 +575,105 @@ def run_ours(args):
     return 0
 
 
+def tc_section(m, policy, device, distributed, times, fallback, args):
+    """configs[4] live: DT (compiled selector over the b200tc classes) vs
+    oracle vs the fp32 default tile vs the best single tc tile, on the
+    held-out random shapes; roofline of the dominant tensor-core kernel."""
+    from paper_1806_07060_b200 import codegen
+    from paper_1806_07060_b200.kernels import TC_FAMILIES, DeviceCaps, KernelFamily
+
+    tcm = build_tc_model(policy)
+    if tcm is None:
+        return {"unavailable": f"no {TC_BUNDLE.name}"}
+    runner = Runner(device, DeviceCaps.b200_tc())
+    sel = codegen.CompiledSelector(tcm["tree"], tcm["classes"])
+    cases = [ShapeCase(s, device, keep_host=False) for s in tcm["test"]]
+    reps = max(3, args.steps // 4)
+
+    def timed(how):
+        runs = [times(runner.pass_(cases, how)) for _ in range(reps)]
+        return distributed.reduce_max([statistics.median(r[i] for r in runs) for i in range(len(cases))], device)
+
+    def fixed(cfgs):
+        nat = [c.native() for c in cfgs]
+        return timed(lambda i, c: runner.launch(c, config=nat[i]))
+
+    def dt(i, c):
+        runner.launch(c, selector=sel, fallback=fallback)
+
+    runner.pass_(cases, dt)
+    dt_t = timed(dt)
+    dt_cfgs = [sel.select(*c.shape.mnk) for c in cases]
+    or_cfgs = [tcm["tables"][c.shape.mnk].best_config for c in cases]
+    de_cfgs = [policy.select_config(c.shape) for c in cases]
+    or_t, de_t = fixed(or_cfgs), fixed(de_cfgs)
+    fx_t = fixed([tcm["fixed_tc"]] * len(cases))
+    rate = lambda ts: [c.flops / t / 1e9 for c, t in zip(cases, ts)]  # noqa: E731
+    g_dt, g_or, g_de, g_fx = (geomean(rate(ts)) for ts in (dt_t, or_t, de_t, fx_t))
+    # dominant tensor-core kernel of the DT pass vs the measured bf16 peak
+    tc_idx = [i for i, c in enumerate(dt_cfgs) if c.family in TC_FAMILIES]
+    roof = None
+    if tc_idx:
+        dom = max(tc_idx, key=lambda i: dt_t[i])
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        bf16_peak = float(peaks.get("bf16_tflops", 2250.0))
+        peak = bf16_peak if dt_cfgs[dom].family is KernelFamily.BF16 else bf16_peak / 2
+        ach = cases[dom].flops / dt_t[dom] / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
+                "frac": round(ach / peak, 4), "traffic": None,
+                "kernel": f"{'x'.join(map(str, cases[dom].shape.mnk))}:{dt_cfgs[dom].canonical()}",
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks
+                                else "nominal dense bf16 2250") + ("; tf32 = half of it" if peak != bf16_peak else ""),
+                "note": "event time covers the whole family path (bf16 convert passes included)"}
+    fams = {}
+    for c in dt_cfgs:
+        fams[c.family.value] = fams.get(c.family.value, 0) + 1
+    return {"workload": "random (M,N,K) in 1..8192, 256 shapes seed 1806; held-out 20% (split seed 2024)",
+            "shapes": len(cases), "model": tcm["name"], "n_train": tcm["n_train"], "score_table_mode": tcm["score"],
+            "dt_geomean": round(g_dt, 1), "oracle_geomean": round(g_or, 1), "default_geomean": round(g_de, 1),
+            "fixed_tc_geomean": round(g_fx, 1), "fixed_tc_config": tcm["fixed_tc"].canonical(),
+            "dt_over_oracle": round(g_dt / g_or, 4), "dt_over_default": round(g_dt / g_de, 4),
+            "dt_over_fixed_tc": round(g_dt / g_fx, 4), "dt_families": fams, "roofline": roof,
+            "per_shape": [[list(c.shape.mnk), round(a, 1), round(b, 1), d.canonical(), o.canonical()]
+                          for c, a, b, d, o in zip(cases, rate(dt_t), rate(or_t), dt_cfgs, or_cfgs)]}
+
+
+def sweep_section(device, distributed, rank, world):
+    """configs[3]: the exhaustive tuning sweep (B200 profile, timing 1 + 3,
+    the sweep the shipped tables came from) over a fixed 16-shape set
+    (M = N and K in {128, 256, 512, 1024}), LPT-sharded shape-wise over the
+    ranks with no collective (cli tune --gpus); wall time = max over ranks.
+    Total work is fixed, so this sub-measurement scales strongly."""
+    import torch
+
+    from paper_1806_07060_b200 import distributed as dist_mod
+    from paper_1806_07060_b200.kernels import DeviceCaps, ProblemShape, full_search_space
+    from paper_1806_07060_b200.sharding import sweep_cost
+    from paper_1806_07060_b200.tuner import TimingPolicy, tune_exhaustive
+
+    caps = DeviceCaps.b200()
+    timing = TimingPolicy(warmup=1, repeats=3)
+    dims = (128, 256, 512, 1024)
+    shapes = [ProblemShape(mn, mn, k) for mn in dims for k in dims]
+    n_cfg = len(full_search_space(caps))
+    mine = dist_mod.shard(shapes, rank, world, lambda s: sweep_cost(s.mnk, n_cfg, 8))
+    tune_exhaustive(ProblemShape(64, 64, 64), caps, timing)  # warm every kernel once
+    distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in mine:
+        tune_exhaustive(s, caps, timing)
+    torch.cuda.synchronize()
+    wall = distributed.reduce_max([time.perf_counter() - t0], device)[0]
+    flops = sum(2.0 * s.M * s.N * s.K for s in shapes)
+    return {"shapes": len(shapes), "configs_per_shape": n_cfg, "configs_timed": n_cfg * len(shapes),
+            "wall_s": round(wall, 3), "configs_per_s": round(n_cfg * len(shapes) / wall, 1),
+            "shapes_per_s": round(len(shapes) / wall, 3), "ranks": world, "scaling": "strong",
+            "swept_tflop": round(flops * n_cfg / 1e12, 3),
+            "how": "tune_exhaustive per shape on this rank's LPT shard; wall clock around the shard, "
+                   "max over ranks (device-timed samples inside, CUDA events)"}
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -530,6 +681,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the sharded-sweep sub-measurement")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rules)")

@@ -280,9 +280,13 @@ int ag_is_legal(const ag_config* c, const ag_caps* caps) {
         // spaces.is_legal_tuple: tensor-core resources are TMEM and the
         // stage ring, not the CUDA-core register / tile caps
         const int bk = c->family == AG_FAMILY_TF32 ? 32 : 64;
-        const int64_t smem = (int64_t)c->tm * (128 + c->bn) * 128 + 1024 + 256;
-        return c->bm == 128 && c->bk == bk && c->tn == 1 && c->uk == 1 && c->bn % 32 == 0 && c->bn >= 32 &&
-               c->bn <= 256 && c->tm >= 2 && c->tm <= 8 && smem <= 227 * 1024;
+        const int chunk = c->family == AG_FAMILY_TF32 ? 32 : 64;
+        if ((c->bm != 128 && c->bm != 256) || c->bk != bk || c->tn != 1 || c->uk != 1) return 0;
+        if (c->bn % 32 || c->bn < 32 || c->bn > 256 || c->tm < 2 || c->tm > 8) return 0;
+        const int ctas = c->bm / 128;
+        if (ctas == 2 && (c->bn / 2) % chunk) return 0;
+        const int64_t smem = (int64_t)c->tm * (128 + c->bn / ctas) * 128 + 1024 + 256;
+        return smem <= 227 * 1024;
     }
     if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT && c->family != AG_FAMILY_SPLITK) return 0;
     if (c->family == AG_FAMILY_DIRECT && c->uk != 1) return 0;

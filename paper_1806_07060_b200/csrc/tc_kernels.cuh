@@ -122,11 +122,11 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_byte
 }
 
 // instruction descriptor: D f32, A/B format, A/B major (0 = K, 1 = MN),
-// N >> 3, M >> 4
+// N >> 3, M >> 4 (M = 128 per CTA, 256 for a CTA pair)
 template <int KIND>
-__host__ __device__ constexpr uint32_t instr_desc(int n, int a_mn, int b_mn) {
+__host__ __device__ constexpr uint32_t instr_desc(int m, int n, int a_mn, int b_mn) {
     return (1u << 4) | (Elem<KIND>::FMT << 7) | (Elem<KIND>::FMT << 10) | ((uint32_t)a_mn << 15) |
-           ((uint32_t)b_mn << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+           ((uint32_t)b_mn << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 template <int KIND>
@@ -189,25 +189,82 @@ constexpr uint32_t tmem_cols() {
                                      : (ACC_STAGES * BN) <= 256 ? 256 : 512;
 }
 
-template <int BN, int STAGES>
+// per-CTA shared memory: the stage ring (A: 128 rows, B: BN / CTAS rows of
+// 128 bytes per stage) + alignment slack + barriers
+template <int BN, int STAGES, int CTAS>
 constexpr size_t smem_bytes() {
-    return 1024 /* alignment slack */ + (size_t)STAGES * (BM + BN) * ROW_BYTES + 256 /* barriers */;
+    return 1024 + (size_t)STAGES * (BM + BN / CTAS) * ROW_BYTES + 256;
 }
 
-template <int KIND, int BN, int STAGES>
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// 2-CTA TMA: lands in this CTA's shared memory, completes the transaction
+// on the leader CTA's barrier (shared::cluster address with the peer bit
+// cleared)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int x,
+                                                 int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];\n" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
+        : "memory");
+}
+template <int KIND>
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {
+    if constexpr (KIND == KIND_TF32) {
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+            " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+    } else {
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+            " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+    }
+}
+// commit the pair's MMAs to the same barrier offset in both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            smem_addr(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(smem_addr(bar)), "r"(cta));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+}
+
+// CTAS = 1: one CTA per SM, UMMA M = 128.  CTAS = 2: a CTA pair on the two
+// SMs of a TPC (cluster of 2) runs tcgen05.mma.cta_group::2 with M = 256:
+// each CTA stages its own 128 rows of A and half of the BN columns of B,
+// the leader CTA issues the MMAs for both, and each CTA's TMEM holds its
+// 128 output rows.  Per SM this halves the B traffic of a 128 x BN tile.
+template <int KIND, int BN, int STAGES, int CTAS>
 __global__ void __launch_bounds__(THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p) {
     constexpr int BK = Elem<KIND>::BK;
-    constexpr uint32_t A_BYTES = BM * ROW_BYTES, B_BYTES = BN * ROW_BYTES;
-    constexpr uint32_t STAGE_TX = A_BYTES + B_BYTES;
+    constexpr int BNC = BN / CTAS;  // B rows (N) staged by each CTA
+    constexpr uint32_t A_BYTES = BM * ROW_BYTES, B_BYTES = BNC * ROW_BYTES;
+    constexpr uint32_t STAGE_TX = (A_BYTES + B_BYTES) * CTAS;
     constexpr uint32_t TMEM_COLS = tmem_cols<BN>();
     constexpr int K_STEPS = BK / Elem<KIND>::UMMA_K;
     constexpr int CH = ROW_BYTES / (int)sizeof(typename Elem<KIND>::T);  // elements per 128-byte MN chunk
     constexpr uint32_t CHUNK_BYTES = BK * ROW_BYTES;                      // one MN chunk of one stage
     constexpr uint32_t MN_SBO = KIND == KIND_TF32 ? 512 : 1024;           // see sw128_desc
     constexpr uint32_t MN_LAYOUT = KIND == KIND_TF32 ? 1 : 2;
-    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 is 16..256 in steps of 16");
-    static_assert(BN % 32 == 0, "epilogue drains 32 columns per tcgen05.ld");
+    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "UMMA N is 16..256; the epilogue drains 32 columns");
+    static_assert(CTAS == 1 || CTAS == 2, "one CTA or a CTA pair");
+    static_assert(BNC % CH == 0 || CTAS == 1, "pair tiles split B into whole 128-byte chunks");
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -220,6 +277,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC_STAGES);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = CTAS == 2 ? cluster_rank() : 0;
+    const int unit = blockIdx.x / CTAS, units = gridDim.x / CTAS;  // one unit = one CTA or one pair
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -229,47 +288,80 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         }
         for (int a = 0; a < ACC_STAGES; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 128);
+            mbar_init(&tempty[a], 4 * CTAS);  // one arrival per epilogue warp of every CTA
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(tmem_slot)),
-                     "n"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+        if constexpr (CTAS == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             smem_addr(tmem_slot)),
+                         "n"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             smem_addr(tmem_slot)),
+                         "n"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CTAS == 2) {
+        cluster_sync();  // the peer's barriers are initialised before any remote arrive
+    } else {
+        __syncthreads();
+    }
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int tiles = p.tiles_m * p.tiles_n;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---- TMA producer
+        if (lane == 0) {  // ---- TMA producer (every CTA stages its own share)
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int t = unit; t < tiles; t += units) {
                 int tm, tn;
                 tile_coords(p, t, tm, tn);
+                const int m0 = tm * BM * CTAS + (int)rank * BM, n0 = tn * BN + (int)rank * BNC;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], STAGE_TX);
                     uint8_t* a = sA + stage * A_BYTES;
                     uint8_t* b = sB + stage * B_BYTES;
-                    if (!p.a_mn) {
-                        tma_load_2d(a, &mapA, &full[stage], kb * BK, tm * BM);
-                    } else {
+                    if constexpr (CTAS == 1) {
+                        mbar_expect_tx(&full[stage], STAGE_TX);
+                        if (!p.a_mn) {
+                            tma_load_2d(a, &mapA, &full[stage], kb * BK, m0);
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < BM / CH; ++c)
-                            tma_load_2d(a + c * CHUNK_BYTES, &mapA, &full[stage], tm * BM + c * CH, kb * BK);
-                    }
-                    if (!p.b_mn) {
-                        tma_load_2d(b, &mapB, &full[stage], kb * BK, tn * BN);
-                    } else {
+                            for (int c = 0; c < BM / CH; ++c)
+                                tma_load_2d(a + c * CHUNK_BYTES, &mapA, &full[stage], m0 + c * CH, kb * BK);
+                        }
+                        if (!p.b_mn) {
+                            tma_load_2d(b, &mapB, &full[stage], kb * BK, n0);
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < BN / CH; ++c)
-                            tma_load_2d(b + c * CHUNK_BYTES, &mapB, &full[stage], tn * BN + c * CH, kb * BK);
+                            for (int c = 0; c < BNC / CH; ++c)
+                                tma_load_2d(b + c * CHUNK_BYTES, &mapB, &full[stage], n0 + c * CH, kb * BK);
+                        }
+                    } else {
+                        const uint32_t bar = smem_addr(&full[stage]) & 0xFEFFFFFFu;  // leader's barrier
+                        if (rank == 0) mbar_expect_tx(&full[stage], STAGE_TX);
+                        if (!p.a_mn) {
+                            tma_load_2d_pair(a, &mapA, bar, kb * BK, m0);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < BM / CH; ++c)
+                                tma_load_2d_pair(a + c * CHUNK_BYTES, &mapA, bar, m0 + c * CH, kb * BK);
+                        }
+                        if (!p.b_mn) {
+                            tma_load_2d_pair(b, &mapB, bar, kb * BK, n0);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < BNC / CH; ++c)
+                                tma_load_2d_pair(b + c * CHUNK_BYTES, &mapB, bar, n0 + c * CH, kb * BK);
+                        }
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -279,10 +371,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
+        if (lane == 0 && rank == 0) {  // ---- MMA issuer (the leader issues for the pair)
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int t = unit; t < tiles; t += units) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + (uint32_t)(acc * BN);
@@ -298,15 +390,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                         const uint64_t bd =
                             p.b_mn ? sw128_desc(b0 + k * Elem<KIND>::UMMA_K * ROW_BYTES, CHUNK_BYTES, MN_SBO, MN_LAYOUT)
                                    : sw128_desc(b0 + k * 32);
-                        umma<KIND>(d, ad, bd, p.idesc, (kb | k) != 0);
+                        if constexpr (CTAS == 1) {
+                            umma<KIND>(d, ad, bd, p.idesc, (kb | k) != 0);
+                        } else {
+                            umma_pair<KIND>(d, ad, bd, p.idesc, (kb | k) != 0);
+                        }
                     }
-                    umma_commit(&empty[stage]);
+                    if constexpr (CTAS == 1) {
+                        umma_commit(&empty[stage]);
+                    } else {
+                        umma_commit_pair(&empty[stage]);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);
+                if constexpr (CTAS == 1) {
+                    umma_commit(&tfull[acc]);
+                } else {
+                    umma_commit_pair(&tfull[acc]);
+                }
                 if (++acc == ACC_STAGES) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -318,12 +422,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         const int row_in_tile = q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int t = unit; t < tiles; t += units) {
             int tm, tn;
             tile_coords(p, t, tm, tn);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int row = tm * BM + row_in_tile;
+            const int row = tm * BM * CTAS + (int)rank * BM + row_in_tile;
             const bool row_ok = row < p.M;
             float* orow = p.out + (i64)row * p.ldo;
             const float* crow = p.C + (i64)row * p.ldc;
@@ -363,7 +467,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0) {
+                    mbar_arrive(&tempty[acc]);
+                } else {
+                    mbar_arrive_remote(&tempty[acc], 0);
+                }
+            }
             if (++acc == ACC_STAGES) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -371,11 +482,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CTAS == 2) {
+        cluster_sync();
+    } else {
+        __syncthreads();
+    }
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(TMEM_COLS)
-                     : "memory");
+        if constexpr (CTAS == 1) {
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(TMEM_COLS)
+                         : "memory");
+        } else {
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(TMEM_COLS)
+                         : "memory");
+        }
     }
 }
 
@@ -538,13 +658,15 @@ inline int stage_operand(const float* src, i64 ld_src, OperandLayout lay, void* 
     return launch_convert<KIND>(static_cast<T*>(ws), *ld, src, ld_src, lay.rows, lay.cols, stream);
 }
 
-template <int KIND, int BN, int STAGES>
+// CTAS = 1: config bm = 128; CTAS = 2: bm = 256 on a CTA pair
+template <int KIND, int BN, int STAGES, int CTAS = 1>
 int launch_tc(const GemmCall& c) {
     typedef typename Elem<KIND>::T T;
     constexpr int BK = Elem<KIND>::BK;
+    constexpr int TILE_M = BM * CTAS;
     if (c.dtype != AG_F32) return tc_fail(c, AG_ERR_CONFIG, "tensor-core families take float32 operands");
     const i64 M = c.M, N = c.N, K = c.K;
-    const i64 tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN, k_blocks = (K + BK - 1) / BK;
+    const i64 tiles_m = (M + TILE_M - 1) / TILE_M, tiles_n = (N + BN - 1) / BN, k_blocks = (K + BK - 1) / BK;
     if (tiles_m * tiles_n > 0x7fffffffLL || k_blocks > 0x7fffffffLL)
         return tc_fail(c, AG_ERR_SHAPE, "problem too large for the tensor-core grid");
     const OperandLayout la = layout_a(M, K, c.ta), lb = layout_b(N, K, c.tb);
@@ -561,11 +683,12 @@ int launch_tc(const GemmCall& c) {
     if ((baseA == (const void*)wsA || baseB == (const void*)wsB) && (c.ws_bytes < need || c.ws == nullptr))
         return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
 
-    // A: K-major unless transA; B: MN-major unless transB
+    // A: K-major unless transA; B: MN-major unless transB.  Boxes are per
+    // CTA: 128 rows of A, BN / CTAS rows of B.
     const int a_mn = c.ta ? 1 : 0, b_mn = c.tb ? 0 : 1;
     CUtensorMap mapA, mapB;
     if (!make_map<KIND>(&mapA, baseA, la.rows, la.cols, ldA, a_mn, BM) ||
-        !make_map<KIND>(&mapB, baseB, lb.rows, lb.cols, ldB, b_mn, BN))
+        !make_map<KIND>(&mapB, baseB, lb.rows, lb.cols, ldB, b_mn, BN / CTAS))
         return tc_fail(c, AG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 
     TcParams p;
@@ -577,7 +700,7 @@ int launch_tc(const GemmCall& c) {
     p.group_m = p.tiles_m < 8 ? p.tiles_m : 8;
     p.a_mn = a_mn;
     p.b_mn = b_mn;
-    p.idesc = instr_desc<KIND>(BN, a_mn, b_mn);
+    p.idesc = instr_desc<KIND>(TILE_M, BN, a_mn, b_mn);
     p.alpha = (float)c.alpha;
     p.beta = (float)c.beta;
     p.use_c = c.beta != 0.0;
@@ -590,17 +713,31 @@ int launch_tc(const GemmCall& c) {
 
     // >= 116 KB of shared memory keeps one CTA per SM, so a CTA never waits
     // on another CTA's TMEM allocation
-    const size_t smem = std::max<size_t>(smem_bytes<BN, STAGES>(), 116 * 1024);
+    const size_t smem = std::max<size_t>(smem_bytes<BN, STAGES, CTAS>(), 116 * 1024);
     if (smem > 227 * 1024) return tc_fail(c, AG_ERR_CONFIG, "config exceeds 227 KB shared memory per CTA");
-    auto kernel = tc_gemm_kernel<KIND, BN, STAGES>;
+    auto kernel = tc_gemm_kernel<KIND, BN, STAGES, CTAS>;
     static std::atomic<int> attr_done{0};
     if (!attr_done.load()) {
         if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return tc_fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
         attr_done.store(1);
     }
-    const unsigned grid = (unsigned)std::min<i64>(tiles_m * tiles_n, sm_count());
-    kernel<<<grid, THREADS, smem, c.stream>>>(mapA, mapB, p);
+    // persistent: one CTA (pair) per SM (TPC), tiles strided over units
+    const i64 units = std::min<i64>(tiles_m * tiles_n, sm_count() / CTAS);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(units * CTAS));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CTAS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kernel, mapA, mapB, p) != cudaSuccess)
+        return tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
     return cudaGetLastError() == cudaSuccess ? AG_OK : tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
 }
 

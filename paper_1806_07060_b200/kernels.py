@@ -205,7 +205,7 @@ INDIRECT_DOMAINS = spaces.INDIRECT_DOMAINS
 
 def domains_for(family: KernelFamily) -> dict[str, tuple[int, ...]]:
     if family in TC_FAMILIES:
-        return {"block_m": (spaces.TC_BLOCK_M,), "block_n": spaces.TC_BLOCK_N,
+        return {"block_m": spaces.TC_BLOCK_M, "block_n": spaces.TC_BLOCK_N,
                 "block_k": (spaces.TC_BLOCK_K[family.value],), "tile_m": spaces.TC_STAGES,
                 "tile_n": (1,), "unroll_k": (1,)}
     if family is KernelFamily.SPLITK:

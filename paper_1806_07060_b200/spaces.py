@@ -53,14 +53,15 @@ SPLITK_BLOCK_K = (16, 32)
 SPLITK_SLICES = (2, 4, 8, 16)
 
 # B200 tensor-core profile ("b200tc"), families "tf32" and "bf16": tcgen05.mma
-# with TMEM accumulators fed by TMA (csrc/tc_kernels.cuh).  bm = 128 is the
-# UMMA M, bn the UMMA N, bk one 128-byte K block (32 tf32 / 64 bf16
-# elements), tm the shared-memory pipeline depth; tn = uk = 1.  They enter
+# with TMEM accumulators fed by TMA (csrc/tc_kernels.cuh).  bm is the UMMA M
+# (128: one CTA per tile; 256: a CTA pair on one TPC, tcgen05 cta_group::2),
+# bn the UMMA N, bk one 128-byte K block (32 tf32 / 64 bf16 elements), tm
+# the shared-memory pipeline depth; tn = uk = 1.  They enter
 # only the b200tc search space: their numerics (tf32 / bf16 inputs, fp32
 # accumulation) differ from the fp32 families, so fp32 tables and trees
 # keep their meaning.
 TC_FAMILIES = ("tf32", "bf16")
-TC_BLOCK_M = 128
+TC_BLOCK_M = (128, 256)
 TC_BLOCK_N = (64, 128, 256)
 TC_BLOCK_K = {"tf32": 32, "bf16": 64}
 TC_STAGES = (2, 3, 4, 6)
@@ -78,9 +79,11 @@ def is_b200_profile(profile) -> bool:
     return profile in (PROFILE_B200, PROFILE_B200_TC)
 
 
-def tc_smem_bytes(bn, stages) -> int:
-    """Dynamic shared memory of one tc CTA: the stage ring + slack + barriers."""
-    return stages * (TC_BLOCK_M + bn) * 128 + 1024 + 256
+def tc_smem_bytes(bm, bn, stages) -> int:
+    """Dynamic shared memory of one tc CTA: the stage ring (128 rows of A and
+    bn / (bm / 128) rows of B per stage) + slack + barriers."""
+    ctas = bm // 128
+    return stages * (128 + bn // ctas) * 128 + 1024 + 256
 
 # DeviceCaps defaults (kernels.py:64-71) and the B200 profile caps
 REFERENCE_CAPS = dict(tile_memory_cap=32768, register_tile_cap_direct=8,
@@ -109,9 +112,14 @@ def is_legal_tuple(family, bm, bn, bk, tm, tn, uk, caps) -> bool:
     if family in TC_FAMILIES:
         # tensor-core resources are TMEM and the stage ring, not the
         # CUDA-core register/tile caps
-        return (bm == TC_BLOCK_M and bk == TC_BLOCK_K[family] and tn == 1 and uk == 1
-                and bn % 32 == 0 and 32 <= bn <= 256 and 2 <= tm <= 8
-                and tc_smem_bytes(bn, tm) <= TC_SMEM_LIMIT)
+        if bm not in TC_BLOCK_M or bk != TC_BLOCK_K[family] or tn != 1 or uk != 1:
+            return False
+        if bn % 32 or not 32 <= bn <= 256 or not 2 <= tm <= 8:
+            return False
+        # a pair splits B into whole 128-byte chunks per CTA (64 bf16 / 32 tf32)
+        if bm == 256 and (bn // 2) % (128 // (2 if family == "bf16" else 4)):
+            return False
+        return tc_smem_bytes(bm, bn, tm) <= TC_SMEM_LIMIT
     if family == "direct" and uk != 1:
         return False
     if family == "splitk":
@@ -144,8 +152,8 @@ def enumerate_tuples(family, caps, profile=PROFILE_REFERENCE):
     if family in TC_FAMILIES:
         if profile != PROFILE_B200_TC:
             return []
-        return [t for bn in TC_BLOCK_N for st in TC_STAGES
-                for t in [(family, TC_BLOCK_M, bn, TC_BLOCK_K[family], st, 1, 1)] if is_legal_tuple(*t, caps)]
+        return [t for bm in TC_BLOCK_M for bn in TC_BLOCK_N for st in TC_STAGES
+                for t in [(family, bm, bn, TC_BLOCK_K[family], st, 1, 1)] if is_legal_tuple(*t, caps)]
     if family == "splitk":
         if not is_b200_profile(profile):
             return []

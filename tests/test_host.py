@@ -14,7 +14,7 @@ import shutil
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, golden
+from conftest import GOLDEN, ROOT, golden
 from oracle import cart as ocart
 from paper_1806_07060_b200 import codegen, evaluation, rng, sharding
 from paper_1806_07060_b200 import model as M
@@ -565,3 +565,32 @@ def test_lpt_partition_properties():
         biggest = max(sharding.sweep_cost(t, 576) for t in shapes)
         assert max(loads) - min(loads) <= biggest + 1e-9
     assert sharding.lpt_partition(shapes, 3, lambda t: 1.0) == sharding.lpt_partition(shapes, 3, lambda t: 1.0)
+
+
+def test_gen_random_shapes_deterministic_and_in_range():
+    from paper_1806_07060_b200.dataset import gen_random
+    a = gen_random(64, 1, 8192, 1806)
+    b = gen_random(64, 1, 8192, 1806)
+    assert [s.mnk for s in a] == [s.mnk for s in b]
+    assert len({s.mnk for s in a}) == 64
+    assert all(1 <= d <= 8192 for s in a for d in s.mnk)
+    assert [s.mnk for s in gen_random(64, 1, 8192, 7)] != [s.mnk for s in a]
+    # first draws: M, N, K in order from one SplitMix64 stream
+    g = rng.SplitMix64(1806)
+    assert a[0].mnk == tuple(1 + g.below(8192) for _ in range(3))
+    with pytest.raises(ValueError):
+        gen_random(9, 1, 2, 0)
+
+
+def test_sampling_list_configs_and_tc_config_file():
+    from paper_1806_07060_b200 import cli
+    from paper_1806_07060_b200.kernels import KernelFamily, enumerate_search_space
+    cfg = cli.PipelineConfig.load(ROOT / "configs" / "random_tc_b200.json")
+    assert cfg.caps.profile == "b200tc"
+    shapes, tag = cfg.shapes()
+    assert tag == "random" and len(shapes) == 256
+    picked = cli.sampling_configs(cfg.sampling, cfg.caps)
+    tc = enumerate_search_space(KernelFamily.TF32, cfg.caps) + enumerate_search_space(KernelFamily.BF16, cfg.caps)
+    assert picked[:len(tc)] == tc
+    assert len(picked) == len(set(picked))
+    assert all(c.family not in (KernelFamily.TF32, KernelFamily.BF16) for c in picked[len(tc):])

@@ -87,3 +87,35 @@ def test_workspace_sizes():
     assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(d.native()), 0) == 0
     # Ap: 32 x 64 floats, Bp: 32 x 64 floats, each 256-byte rounded
     assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(i.native()), 0) == 2 * 32 * 64 * 4
+
+
+def test_native_tc_legality_equals_python():
+    lib = _native.lib()
+    ncaps = DeviceCaps.b200_tc().native()
+    for fam in (KernelFamily.TF32, KernelFamily.BF16):
+        for bm in (64, 128, 256):
+            for bn in (16, 32, 64, 96, 128, 192, 256, 288):
+                for bk in (16, 32, 64):
+                    for tm in (1, 2, 4, 6, 7, 8, 9):
+                        for tn, uk in ((1, 1), (2, 1), (1, 2)):
+                            cfg = KernelConfig(fam, bm, bn, bk, tm, tn, uk)
+                            assert bool(lib.ag_is_legal(ctypes.byref(cfg.native()), ctypes.byref(ncaps))) == \
+                                is_legal(cfg, DeviceCaps.b200_tc()), cfg
+
+
+def test_tc_space_has_kernels_float32_only():
+    lib = _native.lib()
+    tc = [c for c in full_search_space(DeviceCaps.b200_tc()) if c.family in (KernelFamily.TF32, KernelFamily.BF16)]
+    assert len(tc) >= 30
+    assert {c.block_m for c in tc} == {128, 256}  # one CTA and CTA-pair (cta_group::2) tiles
+    for cfg in tc:
+        assert lib.ag_has_kernel(ctypes.byref(cfg.native()), _native.AG_F32), cfg
+
+
+def test_tc_workspace_sizes():
+    lib = _native.lib()
+    cfg = KernelConfig(KernelFamily.BF16, 128, 128, 64, 4, 1, 1)
+    s = native_shape(ProblemShape(33, 70, 17))
+    # bf16 staging keeps the layout: A 33 x 24 (17 -> 8-multiple), B 17 x 72, each 1 KiB rounded
+    want = -(-33 * 24 * 2 // 1024) * 1024 + -(-17 * 72 * 2 // 1024) * 1024
+    assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(cfg.native()), 0) == want
