@@ -594,3 +594,19 @@ def test_sampling_list_configs_and_tc_config_file():
     assert picked[:len(tc)] == tc
     assert len(picked) == len(set(picked))
     assert all(c.family not in (KernelFamily.TF32, KernelFamily.BF16) for c in picked[len(tc):])
+
+
+def test_merge_tables_keeps_base_and_order():
+    from paper_1806_07060_b200.kernels import KernelConfig, ProblemShape
+    from paper_1806_07060_b200.tuner import Measurement, TuningTable, merge_tables
+    s = ProblemShape(64, 64, 64)
+    c1, c2, c3 = (KernelConfig.from_canonical(x) for x in
+                  ("direct:8-8-8-1-1-1", "bf16:128-64-64-2-1-1", "bf16:256-128-64-2-1-1"))
+    meta = {"warmup": "1", "repeats": "3", "timer": "cuda-events"}
+    a = TuningTable.from_measurements(s, [Measurement(c1, 1.0, 1.0), Measurement(c2, 0.5, 2.0)], meta)
+    b = TuningTable.from_measurements(s, [Measurement(c3, 0.25, 4.0), Measurement(c2, 0.1, 9.0)], meta)
+    m = merge_tables(a, b, order=[c2, c3, c1])
+    assert [x.config for x in m.measurements] == [c2, c3, c1]
+    assert m.find(c2).gflops == 2.0 and m.best_config == c3
+    with pytest.raises(ValueError):
+        merge_tables(a, TuningTable.from_measurements(s, [Measurement(c3, 1.0, 1.0)], dict(meta, repeats="5")))
