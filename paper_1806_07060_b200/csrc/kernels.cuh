@@ -64,6 +64,86 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __device__ __forceinline__ float fmadd(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fmadd(double a, double b, double c) { return __fma_rn(a, b, c); }
 
+// Packed fp32 pairs for the sm_100 paired FMA (fma.rn.f32x2 -> SASS FFMA2).
+// One FFMA2 does two IEEE fp32 FMAs (each rounded once, exactly as two
+// fma.rn.f32), so the per-element operation sequence -- and the result -- is
+// unchanged.  With a scalar first operand ptxas emits the broadcast form
+// `FFMA2 Rd, Ra.F32, Rb.F32x2, Rc.F32x2`: a register tile updated as
+// acc[i][j:j+2] += a[i] * b[j:j+2] issues half the instructions of the
+// scalar loop, and every pair operand spans both register banks, which
+// removes the bank-conflict dispatch stalls of the 3-register FFMA.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ void ffma2(f32x2& d, float a, f32x2 b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(pack2(a, a)), "l"(b));
+}
+
+// Register tile acc[TM][TN] += a[TM] (x) b[TN].  For fp32 with an even TN the
+// tile is held as TM x TN/2 packed pairs and updated with FFMA2; otherwise
+// scalar FMAs.  Same products, same per-element order either way.
+template <typename T, int TM, int TN>
+struct RegTile {
+    static constexpr bool PAIRED = false;
+    T acc[TM][TN];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+    }
+    __device__ __forceinline__ void fma(const T (&a)[TM], const T (&b)[TN]) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fmadd(a[i], b[j], acc[i][j]);
+    }
+    __device__ __forceinline__ void unpack(T (&out)[TM][TN]) const {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) out[i][j] = acc[i][j];
+    }
+};
+
+template <int TM, int TN>
+struct RegTilePaired {
+    static constexpr bool PAIRED = true;
+    f32x2 acc[TM][TN / 2];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN / 2; ++j) acc[i][j] = 0ull;
+    }
+    __device__ __forceinline__ void fma(const float (&a)[TM], const float (&b)[TN]) {
+        f32x2 bp[TN / 2];
+#pragma unroll
+        for (int j = 0; j < TN / 2; ++j) bp[j] = pack2(b[2 * j], b[2 * j + 1]);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN / 2; ++j) ffma2(acc[i][j], a[i], bp[j]);
+    }
+    __device__ __forceinline__ void unpack(float (&out)[TM][TN]) const {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN / 2; ++j) unpack2(acc[i][j], out[i][2 * j], out[i][2 * j + 1]);
+    }
+};
+
+template <typename T, int TM, int TN, bool OK = (sizeof(T) == 4 && TN % 2 == 0)>
+struct RegTileFor { typedef RegTile<T, TM, TN> type; };
+template <int TM, int TN>
+struct RegTileFor<float, TM, TN, true> { typedef RegTilePaired<TM, TN> type; };
+
 // Interleaved register-tile layout: thread t (of TT along a dimension) owns
 // elements g*TT*W + t*W + e for g < TILE/W, e < W.  Consecutive threads read
 // consecutive W-vectors, so a warp's LDS.64/LDS.128 phases are conflict free.
@@ -163,11 +243,8 @@ direct_gemm_kernel(const DirectParams<T> p) {
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int M = p.M, N = p.N, K = p.K;
 
-    T acc[TM][TN];
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+    typename RegTileFor<T, TM, TN>::type rt;
+    rt.zero();
 
     auto load_tile = [&](int kt, int s) {
         const int k0 = kt * BK;
@@ -224,13 +301,12 @@ direct_gemm_kernel(const DirectParams<T> p) {
             T a[TM], b[TN];
             load_frag<T, TM, WA>(a, as + k * LA, ty, TY);
             load_frag<T, TN, WB>(b, bs + k * LB, tx, TX);
-#pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-                for (int j = 0; j < TN; ++j) acc[i][j] = fmadd(a[i], b[j], acc[i][j]);
+            rt.fma(a, b);
         }
         __syncthreads();
     }
+    T acc[TM][TN];
+    rt.unpack(acc);
 
     // out = alpha * acc + beta * C, C always read (kernels.py:227)
 #pragma unroll
@@ -294,11 +370,8 @@ tiled_gemm_kernel(const TiledParams<T> p) {
     }
     const int m0 = tm_idx * BM, n0 = tn_idx * BN;
 
-    T acc[TM][TN];
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+    typename RegTileFor<T, TM, TN>::type rt;
+    rt.zero();
 
     // K-major packed A: row k of the tile is contiguous; row-major A (AROW):
     // row i of the tile is contiguous along k
@@ -390,11 +463,7 @@ tiled_gemm_kernel(const TiledParams<T> p) {
                     load_frag<T, TN, WB>(b[u], bs + (k + u) * BN, tx, TX);
                 }
 #pragma unroll
-                for (int u = 0; u < UK; ++u)
-#pragma unroll
-                    for (int i = 0; i < TM; ++i)
-#pragma unroll
-                        for (int j = 0; j < TN; ++j) acc[i][j] = fmadd(a[u][i], b[u][j], acc[i][j]);
+                for (int u = 0; u < UK; ++u) rt.fma(a[u], b[u]);
             }
         } else {
             for (int k = 0; k < BK; k += uk) {
@@ -402,15 +471,14 @@ tiled_gemm_kernel(const TiledParams<T> p) {
                     T a[TM], b[TN];
                     load_frag<T, TM, WA>(a, as + (k + u) * BM, ty, TY);
                     load_frag<T, TN, WB>(b, bs + (k + u) * BN, tx, TX);
-#pragma unroll
-                    for (int i = 0; i < TM; ++i)
-#pragma unroll
-                        for (int j = 0; j < TN; ++j) acc[i][j] = fmadd(a[i], b[j], acc[i][j]);
+                    rt.fma(a, b);
                 }
             }
         }
     }
     cp_async_wait<0>();
+    T acc[TM][TN];
+    rt.unpack(acc);
 
     if (p.splits > 1) {
         // split-K: raw partial sums into this slice's padded Mp x Np slab;

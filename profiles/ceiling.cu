@@ -1,0 +1,92 @@
+// ceiling.cu -- FP32 ceilings for the roofline discussion (measurement only,
+// not product code).  Built into profiles/_ceiling.so by profiles/fp32_ceiling.py.
+//
+//   smem_outer_kernel<TM,TN>: the indirect core's inner loop with no global
+//   traffic -- per k step TM+TN fragment loads from shared memory (same
+//   interleaved layout, LDS.128) and TM*TN FFMAs on register accumulators --
+//   repeated over a shared-memory-resident 32 x 128 tile pair.  It bounds what
+//   any kernel built on this register tiling can reach.
+#include <cuda_runtime.h>
+
+template <int TM, int TN>
+__global__ void __launch_bounds__((128 / TM) * (128 / TN)) smem_outer_kernel(float* out, int iters) {
+    __shared__ __align__(16) float As[32][128];
+    __shared__ __align__(16) float Bs[32][128];
+    for (int e = threadIdx.x; e < 32 * 128; e += blockDim.x) {
+        (&As[0][0])[e] = 1e-3f * (e % 7);
+        (&Bs[0][0])[e] = 1e-3f * (e % 5);
+    }
+    __syncthreads();
+    constexpr int TX = 128 / TN, TY = 128 / TM;
+    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+    float acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+    int off = 0;
+    for (int it = 0; it < iters; ++it) {
+        // launder a zero offset so the loads are redone every pass, as in
+        // the real kernel (otherwise they would be hoisted out of the loop)
+        asm volatile("" : "+r"(off));
+        const float* pa = &As[0][0] + off;
+        const float* pb = &Bs[0][0] + off;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            float a[TM], b[TN];
+#pragma unroll
+            for (int g = 0; g < TM / 4; ++g) {
+                const float4 v = *reinterpret_cast<const float4*>(pa + k * 128 + g * TY * 4 + ty * 4);
+                a[g * 4] = v.x; a[g * 4 + 1] = v.y; a[g * 4 + 2] = v.z; a[g * 4 + 3] = v.w;
+            }
+#pragma unroll
+            for (int g = 0; g < TN / 4; ++g) {
+                const float4 v = *reinterpret_cast<const float4*>(pb + k * 128 + g * TX * 4 + tx * 4);
+                b[g * 4] = v.x; b[g * 4 + 1] = v.y; b[g * 4 + 2] = v.z; b[g * 4 + 3] = v.w;
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) s += acc[i][j];
+    if (s == 1234.5f) out[0] = s;
+}
+
+extern "C" int smem_outer_tflops(int tm, int tn, int ctas_per_sm, int iters, double* tflops) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    float* out = nullptr;
+    cudaMalloc(&out, sizeof(float));
+    const int threads = (128 / tm) * (128 / tn);
+    const int blocks = sms * ctas_per_sm;
+    auto launch = [&](int n) {
+        if (tm == 8 && tn == 8) smem_outer_kernel<8, 8><<<blocks, threads>>>(out, n);
+        else if (tm == 8 && tn == 4) smem_outer_kernel<8, 4><<<blocks, threads>>>(out, n);
+        else smem_outer_kernel<4, 4><<<blocks, threads>>>(out, n);
+    };
+    launch(4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best = 0.0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        launch(iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double flops = 2.0 * tm * tn * 32.0 * iters * threads * (double)blocks;
+        if (flops / (ms * 1e-3) / 1e12 > best) best = flops / (ms * 1e-3) / 1e12;
+    }
+    cudaFree(out);
+    *tflops = best;
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
