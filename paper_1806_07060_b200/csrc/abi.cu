@@ -285,7 +285,7 @@ int ag_is_legal(const ag_config* c, const ag_caps* caps) {
         if (c->bn % 32 || c->bn < 32 || c->bn > 256 || c->tm < 2 || c->tm > 8) return 0;
         const int ctas = c->bm / 128;
         if (ctas == 2 && (c->bn / 2) % chunk) return 0;
-        const int64_t smem = (int64_t)c->tm * (128 + c->bn / ctas) * 128 + 1024 + 256;
+        const int64_t smem = (int64_t)c->tm * (128 + c->bn / ctas) * 128 + 1024 + (int64_t)ag::tc::EPI_BYTES + 256;
         return smem <= 227 * 1024;
     }
     if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT && c->family != AG_FAMILY_SPLITK) return 0;

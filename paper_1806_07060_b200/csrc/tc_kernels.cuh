@@ -191,9 +191,15 @@ constexpr uint32_t tmem_cols() {
 
 // per-CTA shared memory: the stage ring (A: 128 rows, B: BN / CTAS rows of
 // 128 bytes per stage) + alignment slack + barriers
+// epilogue staging: one 32 x 32 fp32 block per epilogue warp, rows padded
+// to 36 floats (144 bytes: 16-byte aligned rows, conflict-free STS.128 /
+// LDS.128 phases)
+constexpr int EPI_LD = 36;
+constexpr size_t EPI_BYTES = 4 * 32 * EPI_LD * sizeof(float);
+
 template <int BN, int STAGES, int CTAS>
 constexpr size_t smem_bytes() {
-    return 1024 + (size_t)STAGES * (BM + BN / CTAS) * ROW_BYTES + 256;
+    return 1024 + (size_t)STAGES * (BM + BN / CTAS) * ROW_BYTES + EPI_BYTES + 256;
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -270,7 +276,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    float* sEpi = reinterpret_cast<float*>(sB + STAGES * B_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES + EPI_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + ACC_STAGES;
@@ -418,8 +425,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
             }
         }
     } else {  // ---- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+        // Each 32 x 32 block (32 TMEM lanes = output rows, 32 columns) goes
+        // TMEM -> registers (one row per thread) -> this warp's smem block ->
+        // registers (row-contiguous) -> global, so every store instruction
+        // writes whole 128-byte row segments instead of 32 rows x 4/16 bytes.
         const int q = warp & 3;
-        const int row_in_tile = q * 32 + lane;
+        float* blk = sEpi + q * 32 * EPI_LD;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = unit; t < tiles; t += units) {
@@ -427,44 +438,53 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
             tile_coords(p, t, tm, tn);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int row = tm * BM * CTAS + (int)rank * BM + row_in_tile;
-            const bool row_ok = row < p.M;
-            float* orow = p.out + (i64)row * p.ldo;
-            const float* crow = p.C + (i64)row * p.ldc;
+            const int row0 = tm * BM * CTAS + (int)rank * BM + q * 32;  // first row of this warp's block
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
                 const int col0 = tn * BN + c0;
-                if (!row_ok || col0 >= p.N) continue;
-                if (p.vec_out && col0 + 32 <= p.N) {
+                if (row0 >= p.M || col0 >= p.N) continue;  // warp-uniform
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 r;
-                        r.x = p.alpha * __uint_as_float(v[j]);
-                        r.y = p.alpha * __uint_as_float(v[j + 1]);
-                        r.z = p.alpha * __uint_as_float(v[j + 2]);
-                        r.w = p.alpha * __uint_as_float(v[j + 3]);
-                        if (p.use_c) {
-                            const float4 cc = *reinterpret_cast<const float4*>(crow + col0 + j);
-                            r.x += p.beta * cc.x;
-                            r.y += p.beta * cc.y;
-                            r.z += p.beta * cc.z;
-                            r.w += p.beta * cc.w;
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(blk + lane * EPI_LD + j) =
+                        make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                    __uint_as_float(v[j + 3]));
+                __syncwarp();
+                if (p.vec_out && col0 + 32 <= p.N) {
+                    // 8 lanes per row, 4 rows per instruction, float4 each
+                    const int cq = (lane & 7) * 4;
+#pragma unroll
+                    for (int rr = 0; rr < 32; rr += 4) {
+                        const int r = rr + (lane >> 3);
+                        const int row = row0 + r;
+                        if (row < p.M) {
+                            const float4 a = *reinterpret_cast<const float4*>(blk + r * EPI_LD + cq);
+                            float4 o = make_float4(p.alpha * a.x, p.alpha * a.y, p.alpha * a.z, p.alpha * a.w);
+                            if (p.use_c) {
+                                const float4 cc = *reinterpret_cast<const float4*>(p.C + (i64)row * p.ldc + col0 + cq);
+                                o.x += p.beta * cc.x;
+                                o.y += p.beta * cc.y;
+                                o.z += p.beta * cc.z;
+                                o.w += p.beta * cc.w;
+                            }
+                            *reinterpret_cast<float4*>(p.out + (i64)row * p.ldo + col0 + cq) = o;
                         }
-                        *reinterpret_cast<float4*>(orow + col0 + j) = r;
                     }
                 } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = col0 + j;
-                        if (col < p.N) {
-                            float r = p.alpha * __uint_as_float(v[j]);
-                            if (p.use_c) r += p.beta * crow[col];
-                            orow[col] = r;
+                    // one row per instruction, lane = column
+                    const int col = col0 + lane;
+#pragma unroll 4
+                    for (int r = 0; r < 32; ++r) {
+                        const int row = row0 + r;
+                        if (row < p.M && col < p.N) {
+                            float o = p.alpha * blk[r * EPI_LD + lane];
+                            if (p.use_c) o += p.beta * p.C[(i64)row * p.ldc + col];
+                            p.out[(i64)row * p.ldo + col] = o;
                         }
                     }
                 }
+                __syncwarp();
             }
             tc_fence_before();
             __syncwarp();
@@ -609,9 +629,12 @@ struct OperandLayout {
 inline OperandLayout layout_a(i64 M, i64 K, int ta) { return ta ? OperandLayout{K, M} : OperandLayout{M, K}; }
 inline OperandLayout layout_b(i64 N, i64 K, int tb) { return tb ? OperandLayout{N, K} : OperandLayout{K, N}; }
 
+// staged rows start on 128-byte boundaries, so every TMA box row is one
+// whole L2 line (a 16-byte-aligned but line-straddling stride costs a
+// second line per row)
 template <int KIND>
 inline i64 staged_ld(i64 cols) {
-    return round_up_i(cols, 16 / (i64)sizeof(typename Elem<KIND>::T));
+    return round_up_i(cols, ROW_BYTES / (i64)sizeof(typename Elem<KIND>::T));
 }
 
 // [A staging | B staging], each 1024-byte aligned: converted (bf16) or

@@ -79,11 +79,14 @@ def is_b200_profile(profile) -> bool:
     return profile in (PROFILE_B200, PROFILE_B200_TC)
 
 
+TC_EPILOGUE_BYTES = 4 * 32 * 36 * 4  # per-warp 32 x 32 fp32 staging blocks (tc_kernels.cuh EPI_BYTES)
+
+
 def tc_smem_bytes(bm, bn, stages) -> int:
     """Dynamic shared memory of one tc CTA: the stage ring (128 rows of A and
-    bn / (bm / 128) rows of B per stage) + slack + barriers."""
+    bn / (bm / 128) rows of B per stage) + slack + epilogue staging + barriers."""
     ctas = bm // 128
-    return stages * (128 + bn // ctas) * 128 + 1024 + 256
+    return stages * (128 + bn // ctas) * 128 + 1024 + TC_EPILOGUE_BYTES + 256
 
 # DeviceCaps defaults (kernels.py:64-71) and the B200 profile caps
 REFERENCE_CAPS = dict(tile_memory_cap=32768, register_tile_cap_direct=8,

@@ -8,7 +8,7 @@
 //   any kernel built on this register tiling can reach.
 #include <cuda_runtime.h>
 
-template <int TM, int TN>
+template <int TM, int TN, bool PAIRED>
 __global__ void __launch_bounds__((128 / TM) * (128 / TN)) smem_outer_kernel(float* out, int iters) {
     __shared__ __align__(16) float As[32][128];
     __shared__ __align__(16) float Bs[32][128];
@@ -44,10 +44,24 @@ __global__ void __launch_bounds__((128 / TM) * (128 / TN)) smem_outer_kernel(flo
                 const float4 v = *reinterpret_cast<const float4*>(pb + k * 128 + g * TX * 4 + tx * 4);
                 b[g * 4] = v.x; b[g * 4 + 1] = v.y; b[g * 4 + 2] = v.z; b[g * 4 + 3] = v.w;
             }
+            if (PAIRED) {  // FFMA2, scalar-broadcast form (as the product kernels)
 #pragma unroll
-            for (int i = 0; i < TM; ++i)
+                for (int i = 0; i < TM; ++i)
 #pragma unroll
-                for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+                    for (int j = 0; j < TN; j += 2) {
+                        unsigned long long d, x, y;
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(acc[i][j]), "f"(acc[i][j + 1]));
+                        asm("mov.b64 %0, {%1, %1};" : "=l"(x) : "f"(a[i]));
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b[j]), "f"(b[j + 1]));
+                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(x), "l"(y));
+                        asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[i][j]), "=f"(acc[i][j + 1]) : "l"(d));
+                    }
+            } else {
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+            }
         }
     }
     float s = 0.f;
@@ -58,7 +72,7 @@ __global__ void __launch_bounds__((128 / TM) * (128 / TN)) smem_outer_kernel(flo
     if (s == 1234.5f) out[0] = s;
 }
 
-extern "C" int smem_outer_tflops(int tm, int tn, int ctas_per_sm, int iters, double* tflops) {
+extern "C" int smem_outer_tflops(int tm, int tn, int ctas_per_sm, int iters, int paired, double* tflops) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -67,9 +81,15 @@ extern "C" int smem_outer_tflops(int tm, int tn, int ctas_per_sm, int iters, dou
     const int threads = (128 / tm) * (128 / tn);
     const int blocks = sms * ctas_per_sm;
     auto launch = [&](int n) {
-        if (tm == 8 && tn == 8) smem_outer_kernel<8, 8><<<blocks, threads>>>(out, n);
-        else if (tm == 8 && tn == 4) smem_outer_kernel<8, 4><<<blocks, threads>>>(out, n);
-        else smem_outer_kernel<4, 4><<<blocks, threads>>>(out, n);
+        if (paired) {
+            if (tm == 8 && tn == 8) smem_outer_kernel<8, 8, true><<<blocks, threads>>>(out, n);
+            else if (tm == 8 && tn == 4) smem_outer_kernel<8, 4, true><<<blocks, threads>>>(out, n);
+            else smem_outer_kernel<4, 4, true><<<blocks, threads>>>(out, n);
+        } else {
+            if (tm == 8 && tn == 8) smem_outer_kernel<8, 8, false><<<blocks, threads>>>(out, n);
+            else if (tm == 8 && tn == 4) smem_outer_kernel<8, 4, false><<<blocks, threads>>>(out, n);
+            else smem_outer_kernel<4, 4, false><<<blocks, threads>>>(out, n);
+        }
     };
     launch(4);
     cudaEvent_t e0, e1;

@@ -1,0 +1,69 @@
+"""Time candidate indirect-core tiles (profiles/exp_tiles.cu) on tile-multiple
+shapes, plus an RF check against a float64 product (measurement only).
+
+    python profiles/exp_tiles.py          (on the GPU box)
+"""
+import ctypes
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+SHAPES = [(4096, 4096, 4096), (8192, 8192, 8192), (5120, 9216, 2560), (4096, 7168, 4096), (2048, 7168, 2048),
+          (1024, 1024, 1024)]
+
+
+def lib():
+    so = HERE / "_exp_tiles.so"
+    if not so.exists():
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                               "-shared", "-Xcompiler", "-fPIC", f"-I{HERE.parent / 'include'}", "-o", str(so),
+                               str(HERE / "exp_tiles.cu")])
+    L = ctypes.CDLL(str(so))
+    L.exp_ws.restype = ctypes.c_size_t
+    L.exp_ws.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
+    L.exp_time.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                           ctypes.POINTER(ctypes.c_double)]
+    return L
+
+
+def main():
+    import torch
+    L = lib()
+    n = L.exp_count()
+    tiles = []
+    for i in range(n):
+        t = (ctypes.c_int * 6)()
+        L.exp_tile(i, t)
+        tiles.append("-".join(map(str, t)))
+    for (m, nn, k) in SHAPES:
+        a = torch.rand(m, k, device="cuda") - 0.5
+        b = torch.rand(k, nn, device="cuda") - 0.5
+        out = torch.empty(m, nn, device="cuda")
+        ref = None
+        res = {}
+        for i in range(n):
+            ws_n = L.exp_ws(i, m, nn, k)
+            ws = torch.empty(ws_n, dtype=torch.uint8, device="cuda")
+            sec = ctypes.c_double()
+            rc = L.exp_time(i, m, nn, k, a.data_ptr(), b.data_ptr(), out.data_ptr(), ws.data_ptr(), ws_n, 5,
+                            ctypes.byref(sec))
+            if rc:
+                res[tiles[i]] = f"rc={rc}"
+                continue
+            entry = round(2 * m * nn * k / sec.value / 1e12, 2)
+            if m <= 4096 and k <= 4096:
+                if ref is None:
+                    ref = (a.double() @ b.double())
+                rf = float(torch.linalg.norm(out.double() - ref) / torch.linalg.norm(ref))
+                entry = [entry, f"rf={rf:.1e}"]
+            res[tiles[i]] = entry
+        print(json.dumps({"mnk": [m, nn, k], "tflops": res}), flush=True)
+        del a, b, out, ref
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

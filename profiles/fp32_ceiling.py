@@ -30,7 +30,7 @@ def ceiling_lib():
         subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared",
                                "-Xcompiler", "-fPIC", "-o", str(so), str(HERE / "ceiling.cu")])
     lib = ctypes.CDLL(str(so))
-    lib.smem_outer_tflops.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(ctypes.c_double)]
+    lib.smem_outer_tflops.argtypes = [ctypes.c_int] * 5 + [ctypes.POINTER(ctypes.c_double)]
     return lib
 
 
@@ -43,10 +43,12 @@ def main():
     torch.cuda.init()
     print(json.dumps({"probe": "ffma_peak", "tflops": round(ffma_peak_tflops(), 2)}), flush=True)
     lib = ceiling_lib()
-    for tm, tn, c in ((8, 8, 1), (8, 8, 2), (8, 4, 1), (4, 4, 1)):
-        v = ctypes.c_double()
-        lib.smem_outer_tflops(tm, tn, c, 2000, ctypes.byref(v))
-        print(json.dumps({"probe": f"smem_outer {tm}x{tn} @ {c} CTA/SM", "tflops": round(v.value, 2)}), flush=True)
+    for paired in (0, 1):
+        for tm, tn, c in ((8, 8, 1), (8, 8, 2), (8, 4, 1), (4, 4, 1)):
+            v = ctypes.c_double()
+            lib.smem_outer_tflops(tm, tn, c, 2000, paired, ctypes.byref(v))
+            print(json.dumps({"probe": f"smem_outer {tm}x{tn} @ {c} CTA/SM" + (" FFMA2" if paired else " FFMA"),
+                              "tflops": round(v.value, 2)}), flush=True)
 
     torch.backends.cuda.matmul.allow_tf32 = False
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
