@@ -553,8 +553,9 @@ def run_ours(args):
                               "oracle_config", "default_config"],
         "e2e": {"value": round(e2e_value * world, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "how": "codegen.dispatch_native(selector, shape, pinned torch CPU A, B, C, out=pinned): async H2D "
-                       "best of 3 wall-clock calls per shape"},
+                "how": "codegen.dispatch_native(selector, shape, pinned torch CPU A, B, C, out=pinned) -> "
+                       "ag_dispatch_gemm_host: H2D, family path and D2H pipelined over output panels on three "
+                       "streams, one blocking call; best of 3 wall-clock calls per shape"},
         "roofline": {"bound": "fp32-cuda-core (compute)", "achieved": round(achieved, 3),
                      "peak": round(peak_meas, 3), "unit": "TFLOP/s", "frac": round(achieved / peak_meas, 4),
                      "traffic": traffic, "kernel": key,

@@ -113,6 +113,23 @@ int ag_gemm(const ag_shape* shape, const ag_config* config, const ag_caps* caps,
             const void* C, int64_t ldc, void* out, int64_t ldo,
             void* workspace, size_t workspace_bytes, void* stream);
 
+/* replaces kernels.gemm_execute (kernels.py:328-349) as the reference's
+ * callers use it -- HOST operands in, HOST result out (numpy semantics) --
+ * in one blocking call: H2D of op(A), op(B) (and C when the family reads
+ * it), the family path, D2H of out.  The result is cut into `panels` row
+ * panels (M >= N) or column panels (M < N), pipelined over three streams so
+ * the PCIe copies of one panel overlap the kernels of the next; panels <= 0
+ * picks 4 when the call moves >= 32 MB, else 1.  Each panel runs `config`
+ * on a sub-problem with the same rows / columns and K order, so the result
+ * equals ag_gemm's.  Host buffers should be pinned (pageable memory works
+ * but its copies do not overlap).  `device_scratch` holds the staged
+ * operands and the family workspace: ag_host_scratch_bytes(). */
+size_t ag_host_scratch_bytes(const ag_shape* shape, const ag_config* config, int dtype, int panels);
+int ag_gemm_host(const ag_shape* shape, const ag_config* config, const ag_caps* caps, int dtype,
+                 const void* A, int64_t lda, const void* B, int64_t ldb,
+                 const void* C, int64_t ldc, void* out, int64_t ldo,
+                 void* device_scratch, size_t scratch_bytes, int panels, void* stream);
+
 /* ag_gemm timed on the device: `warmup` untimed runs then `repeats` timed
  * samples (CUDA events on `stream`); each sample is the mean of `inner`
  * back-to-back runs replayed from one CUDA graph (inner <= 0: chosen so a
@@ -209,6 +226,16 @@ int ag_dispatch_gemm(const ag_selector* sel, const ag_config* fallback,
                      const void* C, int64_t ldc, void* out, int64_t ldo,
                      void* workspace, size_t workspace_bytes, void* stream,
                      ag_config* selected, int* used_fallback);
+
+/* ag_dispatch_gemm over host operands: select (+ fallback), then
+ * ag_gemm_host with the pick (scratch sized by ag_host_scratch_bytes for
+ * the pick; the codegen.dispatch_and_run path of a numpy caller). */
+int ag_dispatch_gemm_host(const ag_selector* sel, const ag_config* fallback,
+                          const ag_shape* shape, const ag_caps* caps, int dtype,
+                          const void* A, int64_t lda, const void* B, int64_t ldb,
+                          const void* C, int64_t ldc, void* out, int64_t ldo,
+                          void* device_scratch, size_t scratch_bytes, int panels, void* stream,
+                          ag_config* selected, int* used_fallback);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,8 @@ _NP_TO_CODE = {np.dtype(np.float32): 0, np.dtype(np.float64): 1}
 def dtype_code(dtype) -> int:
     """0 float32, 1 float64, -1 anything else (numpy or torch dtype)."""
     t = _torch
+    if t is None and type(dtype).__module__.startswith("torch"):
+        t = torch()  # a torch dtype before this module imported torch
     if t is not None and isinstance(dtype, t.dtype):
         return {t.float32: 0, t.float64: 1}.get(dtype, -1)
     try:

@@ -79,6 +79,11 @@ SIGNATURES = {
     "ag_dispatch_gemm": (c_int, [c_void_p, POINTER(AgConfig), POINTER(AgShape), POINTER(AgCaps), c_int,
                                  _P, c_int64, _P, c_int64, _P, c_int64, _P, c_int64, _P, c_size_t, _P,
                                  POINTER(AgConfig), POINTER(c_int)]),
+    "ag_host_scratch_bytes": (c_size_t, [POINTER(AgShape), POINTER(AgConfig), c_int, c_int]),
+    "ag_gemm_host": (c_int, _GEMM_ARGS[:-1] + [c_int, _P]),
+    "ag_dispatch_gemm_host": (c_int, [c_void_p, POINTER(AgConfig), POINTER(AgShape), POINTER(AgCaps), c_int,
+                                      _P, c_int64, _P, c_int64, _P, c_int64, _P, c_int64, _P, c_size_t, c_int, _P,
+                                      POINTER(AgConfig), POINTER(c_int)]),
 }
 
 _lib = None

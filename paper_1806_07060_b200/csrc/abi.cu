@@ -266,6 +266,88 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, f
     if (s == 1234.5f) out[0] = s;
 }
 
+
+// ------------------------------------------------------------------ host path
+// Host operands (the reference's numpy-in / numpy-out gemm_execute): the
+// result is split into panels -- row panels of out when M >= N (B crosses
+// once, A / C / out stream by rows), else column panels (A crosses once,
+// B / C / out stream by columns).  Three streams pipeline panel p's H2D,
+// panel p-1's family path and panel p-2's D2H, so the PCIe copies overlap
+// the kernels.  Every panel runs the same config on a sub-problem whose
+// output elements see exactly the rows of op(A) / columns of op(B) and the
+// K order of the whole call, so the result equals the one-shot call's.
+struct HostPipe {
+    cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> ev;
+    bool ok() {
+        for (auto& x : s)
+            if (!x && cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return false;
+        return true;
+    }
+    cudaEvent_t event(size_t i) {
+        while (ev.size() <= i) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+            ev.push_back(e);
+        }
+        return ev[i];
+    }
+};
+thread_local HostPipe t_pipe;
+
+constexpr int64_t kHostAlign = 256;
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct HostPlan {
+    bool by_rows;          // split M (else N)
+    int64_t extent, chunk;  // split dimension and panel width
+    int panels;
+    bool reads_c;
+    int64_t elem;
+    int64_t ra, ca, rb, cb;  // stored shapes of A and B
+    size_t offA, offB, offC, offO, offW, wsz, total;
+};
+
+bool plan_host(const ag_shape* s, const ag_config* c, int dtype, int panels, HostPlan* h) {
+    h->elem = dtype == AG_F64 ? 8 : 4;
+    h->by_rows = s->m >= s->n;
+    h->extent = h->by_rows ? s->m : s->n;
+    // auto: ~4 panels once the call moves >= 32 MB, never panels under 256
+    const int64_t bytes = (s->m * s->k + s->k * s->n + 2 * s->m * s->n) * h->elem;
+    int p = panels > 0 ? panels : (bytes >= (32LL << 20) ? 4 : 1);
+    int64_t chunk = align_up((h->extent + p - 1) / p, 256);
+    if (chunk >= h->extent) chunk = h->extent;
+    h->chunk = chunk;
+    h->panels = (int)((h->extent + chunk - 1) / chunk);
+    h->reads_c = s->beta != 0.0 || c->family == AG_FAMILY_DIRECT;  // direct always reads C (kernels.py:227)
+    h->ra = s->trans_a ? s->k : s->m;
+    h->ca = s->trans_a ? s->m : s->k;
+    h->rb = s->trans_b ? s->n : s->k;
+    h->cb = s->trans_b ? s->k : s->n;
+    // workspace of the largest panel
+    ag_shape ps = *s;
+    if (h->by_rows) ps.m = chunk; else ps.n = chunk;
+    h->wsz = ag_workspace_bytes(&ps, c, dtype);
+    size_t off = 0;
+    auto take = [&](int64_t n) { size_t o = off; off += (size_t)align_up(n, kHostAlign); return o; };
+    h->offA = take(h->ra * h->ca * h->elem);
+    h->offB = take(h->rb * h->cb * h->elem);
+    h->offC = take(h->reads_c ? s->m * s->n * h->elem : 0);
+    h->offO = take(s->m * s->n * h->elem);
+    h->offW = take((int64_t)h->wsz);
+    h->total = off;
+    return true;
+}
+
+// rows x width_bytes block between pitched buffers
+inline cudaError_t copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t rows,
+                          cudaMemcpyKind kind, cudaStream_t st) {
+    if (rows <= 0 || width <= 0) return cudaSuccess;
+    if ((dpitch == width && spitch == width) || rows == 1)  // one contiguous run: a plain copy
+        return cudaMemcpyAsync(dst, src, (size_t)(width * rows), kind, st);
+    return cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)rows, kind, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -327,6 +409,111 @@ int ag_gemm(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtyp
     int r = prepare(s, c, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, &fn);
     if (r) return r;
     return fn(make_call(s, c, dtype, A, lda, B, ldb, C, ldc, out, ldo, ws, ws_bytes, stream));
+}
+
+size_t ag_host_scratch_bytes(const ag_shape* s, const ag_config* c, int dtype, int panels) {
+    if (!s || !c || s->m < 1 || s->n < 1 || s->k < 1) return 0;
+    HostPlan h;
+    plan_host(s, c, dtype, panels, &h);
+    return h.total;
+}
+
+int ag_gemm_host(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A, int64_t lda,
+                 const void* B, int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo, void* dev,
+                 size_t dev_bytes, int panels, void* stream) {
+    ag::LaunchFn fn = nullptr;
+    int r = prepare(s, c, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, &fn);
+    if (r) return r;
+    HostPlan h;
+    plan_host(s, c, dtype, panels, &h);
+    if (!dev || dev_bytes < h.total) return set_err(AG_ERR_SHAPE, "device scratch too small for the host path");
+    if (!t_pipe.ok()) return set_err(AG_ERR_CUDA, "cannot create the host-path streams");
+    cudaStream_t in = t_pipe.s[0], run = t_pipe.s[1], back = t_pipe.s[2];
+    char* base = static_cast<char*>(dev);
+    char *dA = base + h.offA, *dB = base + h.offB, *dC = base + h.offC, *dO = base + h.offO;
+    void* dW = h.wsz ? base + h.offW : nullptr;
+    const int64_t e = h.elem, M = s->m, N = s->n;
+    const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
+    cudaError_t ce = cudaSuccess;
+    auto ok = [&](cudaError_t x) { if (x != cudaSuccess && ce == cudaSuccess) ce = x; };
+    // the caller's stream may still be writing the host buffers' producers
+    cudaEvent_t start = t_pipe.event(0);
+    if (!start) return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
+    ok(cudaEventRecord(start, static_cast<cudaStream_t>(stream)));
+    ok(cudaStreamWaitEvent(in, start, 0));
+    // the operand that is not split crosses once, first
+    if (h.by_rows) {
+        ok(copy2d(dB, h.cb * e, B, ldb * e, h.cb * e, h.rb, H2D, in));
+    } else {
+        ok(copy2d(dA, h.ca * e, A, lda * e, h.ca * e, h.ra, H2D, in));
+    }
+    for (int p = 0; p < h.panels; ++p) {
+        const int64_t x0 = (int64_t)p * h.chunk, w = std::min(h.chunk, h.extent - x0);
+        cudaEvent_t ein = t_pipe.event(1 + 2 * p), edone = t_pipe.event(2 + 2 * p);
+        if (!ein || !edone) return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
+        ag_shape ps = *s;
+        const void *pa, *pb, *pc;
+        void* po;
+        int64_t pla, plb;
+        if (h.by_rows) {  // rows x0 .. x0+w of op(A), C, out
+            if (!s->trans_a) {
+                ok(copy2d(dA + x0 * h.ca * e, h.ca * e, static_cast<const char*>(A) + x0 * lda * e, lda * e,
+                          h.ca * e, w, H2D, in));
+                pa = dA + x0 * h.ca * e;
+            } else {  // stored K x M: a column block
+                ok(copy2d(dA + x0 * e, h.ca * e, static_cast<const char*>(A) + x0 * e, lda * e, w * e, h.ra, H2D, in));
+                pa = dA + x0 * e;
+            }
+            pla = h.ca;
+            pb = dB;
+            plb = h.cb;
+            if (h.reads_c)
+                ok(copy2d(dC + x0 * N * e, N * e, static_cast<const char*>(C) + x0 * ldc * e, ldc * e, N * e, w, H2D,
+                          in));
+            pc = h.reads_c ? (const void*)(dC + x0 * N * e) : (const void*)(dO + x0 * N * e);
+            po = dO + x0 * N * e;
+            ps.m = w;
+        } else {  // columns x0 .. x0+w of op(B), C, out
+            if (!s->trans_b) {  // stored K x N: a column block
+                ok(copy2d(dB + x0 * e, h.cb * e, static_cast<const char*>(B) + x0 * e, ldb * e, w * e, h.rb, H2D, in));
+                pb = dB + x0 * e;
+            } else {  // stored N x K: rows
+                ok(copy2d(dB + x0 * h.cb * e, h.cb * e, static_cast<const char*>(B) + x0 * ldb * e, ldb * e,
+                          h.cb * e, w, H2D, in));
+                pb = dB + x0 * h.cb * e;
+            }
+            plb = h.cb;
+            pa = dA;
+            pla = h.ca;
+            if (h.reads_c)
+                ok(copy2d(dC + x0 * e, N * e, static_cast<const char*>(C) + x0 * e, ldc * e, w * e, M, H2D, in));
+            pc = h.reads_c ? (const void*)(dC + x0 * e) : (const void*)(dO + x0 * e);
+            po = dO + x0 * e;
+            ps.n = w;
+        }
+        ok(cudaEventRecord(ein, in));
+        ok(cudaStreamWaitEvent(run, ein, 0));
+        r = fn(make_call(&ps, c, dtype, pa, pla, pb, plb, pc, N, po, N, dW, h.wsz, run));
+        if (r) {
+            cudaStreamSynchronize(in);
+            cudaStreamSynchronize(run);
+            cudaStreamSynchronize(back);
+            return r;
+        }
+        ok(cudaEventRecord(edone, run));
+        ok(cudaStreamWaitEvent(back, edone, 0));
+        if (h.by_rows) {
+            ok(copy2d(static_cast<char*>(out) + x0 * ldo * e, ldo * e, dO + x0 * N * e, N * e, N * e, w, D2H, back));
+        } else {
+            ok(copy2d(static_cast<char*>(out) + x0 * e, ldo * e, dO + x0 * e, N * e, w * e, M, D2H, back));
+        }
+    }
+    ok(cudaStreamSynchronize(back));
+    ok(cudaStreamSynchronize(run));
+    ok(cudaStreamSynchronize(in));
+    if (ce != cudaSuccess) return set_err(AG_ERR_CUDA, std::string("host path: ") + cudaGetErrorString(ce));
+    cudaError_t le = cudaGetLastError();
+    return le == cudaSuccess ? AG_OK : set_err(AG_ERR_CUDA, cudaGetErrorString(le));
 }
 
 int ag_gemm_timed(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A, int64_t lda,

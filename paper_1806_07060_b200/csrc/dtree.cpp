@@ -401,4 +401,22 @@ int ag_dispatch_gemm(const ag_selector* sel, const ag_config* fallback, const ag
     return ag_gemm(shape, &pick, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, workspace, workspace_bytes, stream);
 }
 
+int ag_dispatch_gemm_host(const ag_selector* sel, const ag_config* fallback, const ag_shape* shape,
+                          const ag_caps* caps, int dtype, const void* A, int64_t lda, const void* B, int64_t ldb,
+                          const void* C, int64_t ldc, void* out, int64_t ldo, void* device_scratch,
+                          size_t scratch_bytes, int panels, void* stream, ag_config* selected, int* used_fallback) {
+    if (!sel || !shape) return AG_ERR_CONFIG;
+    ag_config pick = sel->cfg[leaf_of(sel, shape->m, shape->n, shape->k)];
+    int fb = 0;
+    if (caps && !ag_is_legal(&pick, caps)) {
+        if (!fallback || !ag_is_legal(fallback, caps)) return AG_ERR_CONFIG;
+        pick = *fallback;
+        fb = 1;
+    }
+    if (selected) *selected = pick;
+    if (used_fallback) *used_fallback = fb;
+    return ag_gemm_host(shape, &pick, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, device_scratch, scratch_bytes,
+                        panels, stream);
+}
+
 }  // extern "C"

@@ -336,6 +336,76 @@ class _Operands:
         return self.out_user
 
 
+class _HostOperands:
+    """Raw host views (pointer, leading dimension) of numpy / torch-CPU
+    operands for the pipelined host path (ag_gemm_host / ag_dispatch_gemm_host).
+    Row-major matrices (unit column stride) are used in place; anything else is
+    copied to a contiguous array first.  `out` is written in place when it is
+    row-major, else through a temporary copied back by result()."""
+
+    def __init__(self, shape: ProblemShape, A, B, C, out):
+        self.code = _device.dtype_code(A.dtype)
+        self._keep = []
+        self.A = self._view(A)
+        self.B = self._view(B)
+        self.C = self._view(C)
+        dt = np.float32 if self.code == 0 else np.float64
+        if out is None:
+            self.out_user = np.empty((shape.M, shape.N), dtype=dt)
+        else:
+            if _dims(out) != (shape.M, shape.N) or _device.dtype_code(out.dtype) != self.code:
+                raise ShapeError("out buffer has wrong shape or dtype")
+            if _device.is_cuda_tensor(out):
+                raise ShapeError("out must be a host buffer when the operands are host buffers")
+            self.out_user = out
+        view = self._view(self.out_user, writable=True)
+        self.out_tmp = None
+        if view is None:  # not row-major: compute into a temporary
+            self.out_tmp = np.empty((shape.M, shape.N), dtype=dt)
+            view = self._view(self.out_tmp, writable=True)
+        self.out = view
+
+    def _view(self, x, writable=False):
+        if _device.is_device_tensor(x):
+            if not (x.dim() == 2 and x.stride(1) == 1 and x.stride(0) >= max(1, x.shape[1])):
+                if writable:
+                    return None
+                x = x.contiguous()
+            self._keep.append(x)
+            return ctypes.c_void_p(x.data_ptr()), max(int(x.stride(0)), int(x.shape[1]), 1)
+        a = np.asarray(x)
+        item = a.dtype.itemsize
+        ok = a.ndim == 2 and (a.shape[1] <= 1 or a.strides[1] == item) and a.strides[0] % item == 0 \
+            and (a.shape[0] <= 1 or a.strides[0] >= a.shape[1] * item)
+        if not ok:
+            if writable:
+                return None
+            a = np.ascontiguousarray(a)
+        if writable and not a.flags.writeable:
+            raise ShapeError("out buffer is read-only")
+        self._keep.append(a)
+        ld = a.strides[0] // item if a.shape[0] > 1 else a.shape[1]
+        return ctypes.c_void_p(a.ctypes.data), max(int(ld), int(a.shape[1]), 1)
+
+    def args(self):
+        return (*self.A, *self.B, *self.C, *self.out)
+
+    def result(self):
+        if self.out_tmp is not None:
+            if _device.is_device_tensor(self.out_user):
+                self.out_user.copy_(_device.torch().from_numpy(self.out_tmp))
+            else:
+                self.out_user[...] = self.out_tmp
+        return self.out_user
+
+
+def host_scratch_bytes(shape: ProblemShape, config: KernelConfig, dtype=np.float32, panels: int = 0) -> int:
+    """Device bytes the pipelined host path needs (staged operands + workspace)."""
+    code = _device.dtype_code(dtype)
+    return int(_native.lib().ag_host_scratch_bytes(ctypes.byref(native_shape(shape)),
+                                                    ctypes.byref(config.native()), max(code, 0), int(panels)))
+
+
 def _raise_for(code: int, config: "KernelConfig | None" = None):
     msg = _native.last_error()
     if code == _native.AG_ERR_CONFIG:

@@ -113,3 +113,77 @@ def test_cli_tune_sharded_workers(tmp_path, capsys):
     assert tables == ["16x16x16.csv", "24x24x24.csv", "32x32x32.csv", "8x8x8.csv"]
     assert main(["tune", "--config", str(cfg), "--gpus", "2", "--force"]) == 0
     assert "0 already done, 4 to run" in capsys.readouterr().out
+
+
+# ---------------------------------------------------------------------------
+# pipelined host path (ag_gemm_host / ag_dispatch_gemm_host): host operands in,
+# host result out; panels must not change a single bit
+
+
+def _one_class_selector(cfg):
+    tree = M.train([((64, 1, 1), 0), ((128, 1, 1), 0)])
+    return codegen.CompiledSelector(tree, {0: cfg})
+
+
+HOST_CASES = [
+    # (M, N, K, alpha, beta, transA, transB, config)
+    (700, 300, 129, 1.0, 0.0, False, False, "indirect:64-64-16-8-4-1"),    # row panels
+    (300, 700, 129, 1.0, 0.0, False, False, "indirect:64-64-16-8-4-1"),    # column panels
+    (517, 211, 77, 1.5, 0.5, True, False, "indirect:32-64-16-4-8-2"),     # transA, beta
+    (211, 517, 77, 1.5, 0.5, False, True, "indirect:64-32-16-8-4-1"),     # transB, beta
+    (333, 333, 64, 1.0, 0.0, True, True, "direct:32-32-16-2-4-1"),        # direct reads C always
+    (1000, 64, 1024, 1.0, 0.0, False, False, "splitk:64-64-16-8-4-8"),    # split-K
+    (600, 520, 300, 1.0, 0.25, False, False, "bf16:256-128-64-4-1-1"),    # tensor-core pair
+    (260, 650, 96, 1.0, 0.0, False, True, "tf32:128-64-32-4-1-1"),
+]
+
+
+@pytest.mark.parametrize("case", HOST_CASES, ids=lambda c: f"{c[0]}x{c[1]}x{c[2]}-{c[7].split(':')[0]}")
+@pytest.mark.parametrize("panels", [1, 3])
+def test_host_path_equals_device_path(case, panels):
+    import torch
+    m, n, k, alpha, beta, ta, tb, name = case
+    cfg = KernelConfig.from_canonical(name)
+    caps = DeviceCaps.b200_tc()
+    s = ProblemShape(m, n, k, alpha=alpha, beta=beta, transA=ta, transB=tb)
+    A, B, C = rand_operands(s, seed=m + n + k)
+    sel = _one_class_selector(cfg)
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+    ref, picked, _ = codegen.dispatch_native(sel, s, dA, dB, dC, caps)
+    ref = ref.cpu().numpy()
+    got, picked_h, fb = codegen.dispatch_native(sel, s, A, B, C, caps, panels=panels)
+    assert picked_h == picked == cfg and not fb
+    assert isinstance(got, np.ndarray)
+    np.testing.assert_array_equal(got, ref)
+    # pinned torch tensors, result into a caller-owned pinned buffer
+    pA, pB, pC = (torch.from_numpy(x).pin_memory() for x in (A, B, C))
+    hout = torch.empty((m, n), dtype=torch.float32).pin_memory()
+    got2, _, _ = codegen.dispatch_native(sel, s, pA, pB, pC, caps, out=hout, panels=panels)
+    assert got2 is hout
+    np.testing.assert_array_equal(hout.numpy(), ref)
+
+
+def test_host_path_strided_operands_and_out():
+    cfg = KernelConfig.from_canonical("indirect:64-64-16-8-4-1")
+    s = ProblemShape(300, 200, 50, alpha=1.0, beta=1.0)
+    A, B, C = rand_operands(s, seed=5)
+    big = np.zeros((300, 260), np.float32)
+    big[:, :50] = A  # row-major view with a leading dimension > K
+    outbuf = np.zeros((200, 300), np.float32).T  # column-major out: written via a temporary
+    sel = _one_class_selector(cfg)
+    got, _, _ = codegen.dispatch_native(sel, s, big[:, :50], B, C, out=outbuf, panels=2)
+    assert got is outbuf
+    ref, _ = gemm_execute(s, cfg, A, B, C)
+    np.testing.assert_array_equal(outbuf, ref)
+
+
+def test_host_path_errors():
+    from paper_1806_07060_b200.kernels import ShapeError
+    cfg = KernelConfig.from_canonical("indirect:64-64-16-8-4-1")
+    s = ProblemShape(30, 20, 10)
+    A, B, C = rand_operands(s, seed=1)
+    sel = _one_class_selector(cfg)
+    with pytest.raises(ShapeError):
+        codegen.dispatch_native(sel, s, A, B, C, out=np.zeros((20, 30), np.float32))
+    with pytest.raises(ShapeError):
+        codegen.dispatch_native(sel, s, A[:, :5], B, C)

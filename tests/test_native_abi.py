@@ -116,6 +116,26 @@ def test_tc_workspace_sizes():
     lib = _native.lib()
     cfg = KernelConfig(KernelFamily.BF16, 128, 128, 64, 4, 1, 1)
     s = native_shape(ProblemShape(33, 70, 17))
-    # bf16 staging keeps the layout: A 33 x 24 (17 -> 8-multiple), B 17 x 72, each 1 KiB rounded
-    want = -(-33 * 24 * 2 // 1024) * 1024 + -(-17 * 72 * 2 // 1024) * 1024
+    # bf16 staging keeps the layout with 128-byte rows: A 33 x 64 (17 -> 64), B 17 x 128 (70 -> 128),
+    # each 1 KiB rounded
+    want = -(-33 * 64 * 2 // 1024) * 1024 + -(-17 * 128 * 2 // 1024) * 1024
     assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(cfg.native()), 0) == want
+
+
+def test_host_scratch_bytes():
+    lib = _native.lib()
+    cfg = KernelConfig(KernelFamily.INDIRECT, 32, 32, 16, 4, 4, 1)
+    shape = ProblemShape(1000, 300, 50)
+    s = native_shape(shape)
+    up = lambda n: -(-n // 256) * 256  # noqa: E731
+    # beta == 0, indirect: staged A, B, out + the workspace of the largest row panel (1 panel: the whole call)
+    ws = lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(cfg.native()), 0)
+    want = up(1000 * 50 * 4) + up(50 * 300 * 4) + up(1000 * 300 * 4) + up(ws)
+    assert lib.ag_host_scratch_bytes(ctypes.byref(s), ctypes.byref(cfg.native()), 0, 1) == want
+    # 4 row panels of 256 rows: workspace of a 256-row panel; the direct family also stages C
+    p = native_shape(ProblemShape(256, 300, 50))
+    ws4 = lib.ag_workspace_bytes(ctypes.byref(p), ctypes.byref(cfg.native()), 0)
+    assert lib.ag_host_scratch_bytes(ctypes.byref(s), ctypes.byref(cfg.native()), 0, 4) == want - up(ws) + up(ws4)
+    d = KernelConfig(KernelFamily.DIRECT, 16, 16, 8, 2, 2, 1)
+    assert lib.ag_host_scratch_bytes(ctypes.byref(s), ctypes.byref(d.native()), 0, 1) == \
+        up(1000 * 50 * 4) + up(50 * 300 * 4) + 2 * up(1000 * 300 * 4)
