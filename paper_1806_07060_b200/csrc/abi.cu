@@ -66,22 +66,28 @@ bool in_range(const ag_config& c) {
            c.bk < 512 && c.tm < 64 && c.tn < 64 && c.uk < 64;
 }
 
-// exact instantiation, else the run-time-tile kernel for (tm, tn); the
-// split-K family runs the indirect core (unroll 1) with a K-slice grid axis
+// exact instantiation, else the run-time-tile kernel for (tm, tn) -- register
+// tiles wider than 8 (the B200 wide tiles in float64, or configs outside the
+// domains) run the 8-wide one: the tile shape only distributes the output
+// elements over threads, every element's K order is the same; the split-K
+// family runs the indirect core (unroll 1) with a K-slice grid axis
 ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
     if (!in_range(c)) return nullptr;
     auto& m = registry().map;
+    const int rtm = std::min(c.tm, 8), rtn = std::min(c.tn, 8);
     if (c.family == AG_FAMILY_SPLITK) {
         auto it = m.find(make_key(AG_FAMILY_SPLITK, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, 0));
         if (it != m.end()) return it->second;
         it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, 1));
         if (it != m.end()) return it->second;
-        it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, 0, 0, 0, c.tm, c.tn, 0));
+        it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, 0, 0, 0, rtm, rtn, 0));
         return it != m.end() ? it->second : nullptr;
     }
     auto it = m.find(make_key(c.family, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk));
     if (it != m.end()) return it->second;
     it = m.find(make_key(c.family, dtype, 0, 0, 0, c.tm, c.tn, 0));
+    if (it != m.end()) return it->second;
+    it = m.find(make_key(c.family, dtype, 0, 0, 0, rtm, rtn, 0));
     if (it != m.end()) return it->second;
     return nullptr;
 }

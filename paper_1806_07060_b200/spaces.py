@@ -42,6 +42,15 @@ B200_INDIRECT_EXTRA_DOMAINS = {
     "unroll_k": (1, 2),
 }
 
+# B200 profile, wide register tiles: 8 x 16 / 16 x 8 accumulators per
+# thread (128 fp32 = 64 FFMA2 pairs), half the shared-memory fragment loads
+# per FMA of an 8 x 8 tile; +3-5 % over 8 x 8 on >= 4096-class shapes
+# (profiles/r01_exp_tiles.jsonl).  An explicit list: each is a compiled
+# kernel, enumerated after the extra domains.
+B200_INDIRECT_WIDE = ((128, 128, 16, 8, 16, 1), (128, 128, 32, 8, 16, 1), (128, 128, 16, 16, 8, 1),
+                      (128, 128, 32, 16, 8, 1), (128, 256, 16, 8, 16, 1), (128, 256, 32, 8, 16, 1),
+                      (256, 128, 16, 16, 8, 1), (256, 128, 32, 16, 8, 1))
+
 # B200 profile, split-K family ("splitk"): the indirect core over `uk` equal
 # K slices plus a fixed-order reduction.  For skinny / small-N shapes whose
 # tile grid cannot fill 148 SMs.  Tiles are ones the indirect family already
@@ -92,7 +101,7 @@ def tc_smem_bytes(bm, bn, stages) -> int:
 REFERENCE_CAPS = dict(tile_memory_cap=32768, register_tile_cap_direct=8,
                       register_tile_cap_indirect=32, element_size=4, max_threads=1024)
 B200_CAPS = dict(tile_memory_cap=65536, register_tile_cap_direct=8,
-                 register_tile_cap_indirect=64, element_size=4, max_threads=1024)
+                 register_tile_cap_indirect=128, element_size=4, max_threads=1024)
 
 REGISTER_FILE = 65536  # 32-bit registers per SM (and per CTA) on sm_100
 
@@ -176,6 +185,11 @@ def enumerate_tuples(family, caps, profile=PROFILE_REFERENCE):
             if is_legal_tuple(*t, caps):
                 out.append(t)
                 seen.add(t)
+        for w in B200_INDIRECT_WIDE:
+            t = ("indirect",) + w
+            if t not in seen and is_legal_tuple(*t, caps):
+                out.append(t)
+                seen.add(t)
     return out
 
 
@@ -196,3 +210,4 @@ def compiled_tuples():
 # register-tile shapes with a run-time-tile-size kernel (any bm/bn/bk):
 # float64 runs these, as do legal float32 configs outside the domains
 RUNTIME_TILES = (1, 2, 4, 8)
+RUNTIME_WIDE_TILES = ((8, 16), (16, 8))  # float64 only (build.py)

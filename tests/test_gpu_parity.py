@@ -225,7 +225,23 @@ def _checksum_ok(s, A, B, C, out, tol=1e-5):
     return rel_frobenius(got, want) <= tol
 
 
+def test_wide_register_tiles_float32_and_float64():
+    """B200 wide tiles (8x16 / 16x8 per thread): their own FFMA2 kernels in
+    float32; float64 runs the 8-wide run-time-tile kernel (same elements)."""
+    from paper_1806_07060_b200.spaces import B200_INDIRECT_WIDE
+    for dt, bar in ((np.float32, 1e-5), (np.float64, 1e-12)):
+        s = ProblemShape(301, 277, 97, alpha=1.5, beta=0.5, transB=True)
+        A, B, C = rand_operands(s, dt, seed=23)
+        ref = _oracle_ref(s, A, B, C)
+        for w in B200_INDIRECT_WIDE:
+            cfg = KernelConfig(KernelFamily.INDIRECT, *w)
+            out, _ = gemm_execute(s, cfg, A, B, C, B200)
+            assert out.dtype == dt
+            assert rel_frobenius(out, ref) <= bar, (cfg.canonical(), dt)
+
+
 @pytest.mark.parametrize("mnk,cfg", [
+    ((5124, 9124, 2560), "indirect:128-256-32-8-16-1"),
     ((4096, 4096, 4096), "indirect:128-128-32-8-8-1"),
     ((5124, 700, 2048), "indirect:128-64-16-8-8-2"),
     ((35, 8457, 2560), "direct:8-32-16-2-4-1"),

@@ -547,7 +547,7 @@ def test_cli_env_caps_override(tmp_path, monkeypatch):
     b = tmp_path / "b.json"
     b.write_text(json.dumps({"caps": {"profile": "b200"}, "dataset": {"strategy": "po2", "min": 64, "max": 64}}))
     pc = PipelineConfig.load(b)
-    assert pc.caps.profile == "b200" and pc.caps.register_tile_cap_indirect == 64
+    assert pc.caps.profile == "b200" and pc.caps.register_tile_cap_indirect == 128
     assert pc.hash() != PipelineConfig.load(cfg).hash()
 
 
