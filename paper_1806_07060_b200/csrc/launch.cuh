@@ -84,8 +84,18 @@ size_t indirect_workspace_bytes(i64 M, i64 N, i64 K, int bm, int bn, int bk, int
     return b;
 }
 
-// L2-friendly tile grouping: ~8 row tiles per group (CUTLASS-style swizzle)
-inline int group_rows(i64 tiles_m) { return (int)(tiles_m < 8 ? tiles_m : 8); }
+// L2-friendly tile grouping (CUTLASS-style swizzle): consecutive CTAs walk
+// `group` row tiles of one column band, so op(B) is streamed from HBM once
+// per group.  The group is as tall as ~32 MB of packed op(A) rows allows
+// (>= 8 tiles), which keeps a group's A panel L2-resident (126 MB) while
+// cutting the B re-reads: 5124 x 9124 x 2560 at 128 x 128 tiles goes from
+// 5 B passes (group 8) to 2 (group 24).
+inline int group_rows(i64 tiles_m, i64 bm, i64 Kp, size_t elem) {
+    const i64 budget = 32LL << 20;
+    i64 g = budget / std::max<i64>(1, bm * Kp * (i64)elem);
+    g = std::max<i64>(g, 8);
+    return (int)std::min<i64>(g, tiles_m);
+}
 
 // AROW_OK (split-K family launchers): when op(A) is the caller's row-major
 // A and M, K are tile multiples, run the AROW core that reads A in place
@@ -173,7 +183,7 @@ int launch_indirect(const GemmCall& c) {
     p.C = static_cast<const T*>(c.C); p.ldc = c.ldc;
     p.out = static_cast<T*>(c.out); p.ldo = c.ldo;
     p.bm = bm; p.bn = bn; p.bk = bk; p.uk = uk;
-    p.tiles_m = (int)tiles_m; p.tiles_n = (int)tiles_n; p.group_m = group_rows(tiles_m);
+    p.tiles_m = (int)tiles_m; p.tiles_n = (int)tiles_n; p.group_m = group_rows(tiles_m, bm, Kp, sizeof(T));
     p.splits = used_splits; p.kt_per_split = kps;
     p.partial = reinterpret_cast<T*>(static_cast<char*>(c.ws) + round_up(Kp * Mp * (i64)sizeof(T), 256) +
                                      round_up(Kp * Np * (i64)sizeof(T), 256));
