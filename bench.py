@@ -194,8 +194,14 @@ def pack_launches(shape, cfg) -> int:
         return 1
     if cfg.family in TC_FAMILIES:  # bf16: one convert pass per operand; tf32 reads fp32 in place
         return 3 if cfg.family is KernelFamily.BF16 else 1
+    arow_fit = not shape.transA and shape.M % cfg.block_m == 0 and shape.K % cfg.block_k == 0
+    if (cfg.family is KernelFamily.SPLITK and not shape.transA and not shape.transB and shape.K % 4 == 0
+            and shape.N % 4 == 0 and (shape.N <= 64 or not arow_fit)):
+        return 1  # in-place core, slices reduced inside the cluster (no packs, no reduce launch)
     n = 1
-    if not (shape.transA and shape.M % cfg.block_m == 0 and shape.K % cfg.block_k == 0):
+    a_in_place = (shape.transA and shape.M % cfg.block_m == 0 and shape.K % cfg.block_k == 0) or \
+        (cfg.family is KernelFamily.SPLITK and arow_fit)
+    if not a_in_place:
         n += 1
     if not (not shape.transB and shape.N % cfg.block_n == 0 and shape.K % cfg.block_k == 0 and shape.N % 4 == 0):
         n += 1
@@ -620,9 +626,13 @@ def tc_section(m, policy, device, distributed, times, fallback, args):
         bf16_peak = float(peaks.get("bf16_tflops", 2250.0))
         peak = bf16_peak if dt_cfgs[dom].family is KernelFamily.BF16 else bf16_peak / 2
         ach = cases[dom].flops / dt_t[dom] / 1e12
+        key = f"{'x'.join(map(str, cases[dom].shape.mnk))}:{dt_cfgs[dom].canonical()}"
+        traffic = json.loads(TRAFFIC_FILE.read_text()).get(key) if TRAFFIC_FILE.exists() else None
         roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
-                "frac": round(ach / peak, 4), "traffic": None,
-                "kernel": f"{'x'.join(map(str, cases[dom].shape.mnk))}:{dt_cfgs[dom].canonical()}",
+                "frac": round(ach / peak, 4), "traffic": traffic,
+                "traffic_note": "DRAM bytes of the tc_gemm launch alone (ncu --set full); the bf16 convert "
+                                "passes add 6 B per operand element",
+                "kernel": key,
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks
                                 else "nominal dense bf16 2250") + ("; tf32 = half of it" if peak != bf16_peak else ""),
                 "note": "event time covers the whole family path (bf16 convert passes included)"}

@@ -1,0 +1,56 @@
+"""Re-time one kernel family over a finished sweep and merge it in.
+
+    python configs/resweep_family.py FAMILY CONFIG.json OLD_TABLES_DIR NEW_TABLES_DIR
+
+For every shape of CONFIG: time the family's configs of the config's search
+space (list mode: the listed ones of that family) with the config's timing
+policy on resident buffers, then write the shape's table with those rows
+replaced (tuner.merge_tables, the re-timed rows win) in the full enumeration
+order.  Used after a kernel change that touches one family only (the
+split-K in-place core), so the other families' measurements are kept.
+"""
+import argparse
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+
+from bundle_tables import full_order  # noqa: E402
+
+from paper_1806_07060_b200 import cli  # noqa: E402
+from paper_1806_07060_b200.kernels import KernelFamily, full_search_space  # noqa: E402
+from paper_1806_07060_b200.tuner import load_table, merge_tables, save_table, table_filename, tune_configs  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("family")
+    ap.add_argument("config")
+    ap.add_argument("old")
+    ap.add_argument("new")
+    a = ap.parse_args()
+    fam = KernelFamily(a.family)
+    cfg = cli.PipelineConfig.load(a.config)
+    shapes, _ = cfg.shapes()
+    order = full_order(cfg) or full_search_space(cfg.caps)
+    mine = [c for c in order if c.family is fam]
+    out = Path(a.new)
+    out.mkdir(parents=True, exist_ok=True)
+    for i, s in enumerate(shapes):
+        dst = out / table_filename(s)
+        if dst.exists():
+            continue
+        old = load_table(Path(a.old) / table_filename(s))
+        fresh = tune_configs(s, mine, cfg.caps, cfg.timing)
+        merged = merge_tables(fresh, old, order)
+        merged.meta.update({k: v for k, v in old.meta.items() if k not in ("configs",)})
+        save_table(merged, dst)
+        if i % 20 == 0:
+            print(f"{i + 1}/{len(shapes)} {s.mnk}: best {merged.best_config.canonical()}", flush=True)
+    print(f"{len(shapes)} tables -> {out}")
+
+
+if __name__ == "__main__":
+    main()

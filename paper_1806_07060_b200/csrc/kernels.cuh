@@ -188,6 +188,7 @@ struct TiledParams {
     int tiles_m, tiles_n, group_m;  // 1-D grid, grouped ("swizzled") tile order
     int splits, kt_per_split;       // split-K: blockIdx.y is the K slice
     T* partial;                     // splits x Mp x Np fp partial sums (splits > 1)
+    int cluster_red;                // in-place core: the slices of a tile are one cluster, reduced over DSMEM
 };
 
 // thread bound of a kernel instantiation: exact for fixed tiles; for the
@@ -531,6 +532,238 @@ tiled_gemm_kernel(const TiledParams<T> p) {
                 if (gn >= p.N) continue;
                 T v = p.alpha * acc[i][j];
                 if (p.use_c) v = fmadd(p.alpha, acc[i][j], p.beta * p.C[(i64)gm * p.ldc + gn]);
+                p.out[(i64)gm * p.ldo + gn] = v;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// in-place core (split-K family): no pack passes.  op(A) = the caller's
+// row-major A and op(B) = the caller's row-major B are streamed with 16-byte
+// cp.async straight from their own layouts, zero-filled past M, N and the
+// slice's K end (K and N multiples of 4, 16-byte aligned rows; the launcher
+// checks).  The A stage is row-major in shared memory ([BM][BK + 4], rows
+// 16-byte aligned, an odd number of 16-byte chunks apart so a warp's
+// LDS.128 / LDS.64 over consecutive rows is conflict free); each thread
+// reads 4 (or 2) k of a row with one load and applies them in k order, so every output
+// element sees exactly the FMA sequence of the packed core: the zero fill is
+// the pack's zero padding, and the result is bit-identical to it.  Thread
+// rows are strided by TY (row r = i * TY + ty), B columns interleaved as in
+// the packed core.
+#ifndef INPLACE_KV
+#define INPLACE_KV 4
+#endif
+template <int BM, int BN, int BK, int TM, int TN, int STAGES>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), ((BM / TM) * (BN / TN) >= 256 && TM * TN <= 64) ? 2 : 1)
+inplace_gemm_kernel(const TiledParams<float> p, int K) {
+    static_assert(BK % 4 == 0 && BN % 4 == 0, "16-byte chunks");
+    constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY;
+    constexpr int LA = BK + 4;  // A stage row stride (floats): 16-byte aligned, odd in chunks when BK % 8 == 0
+    constexpr int WB = FragW<float, TN>::W;
+    constexpr int CA = BM * (BK / 4), CB = BK * (BN / 4);
+    // k values per A fragment load: LDS.128 (4 k) for short register tiles,
+    // LDS.64 (2 k) for TM >= 8, which keeps the 8 x 8 tile at <= 128
+    // registers (two 256-thread CTAs per SM)
+    constexpr int KV = INPLACE_KV;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* As = reinterpret_cast<float*>(smem_raw);  // [STAGES][BM][LA]
+    float* Bs = As + STAGES * BM * LA;                // [STAGES][BK][BN]
+
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
+    int tm_idx, tn_idx;
+    {
+        const int pid = blockIdx.x;
+        const int per_group = p.group_m * p.tiles_n;
+        const int first_m = (pid / per_group) * p.group_m;
+        const int gsz = min(p.tiles_m - first_m, p.group_m);
+        const int r = pid - (pid / per_group) * per_group;
+        tm_idx = first_m + r % gsz;
+        tn_idx = r / gsz;
+    }
+    const int m0 = tm_idx * BM, n0 = tn_idx * BN;
+    const int kt0 = blockIdx.y * p.kt_per_split;
+    const int k_begin = kt0 * BK;
+    const int k_end = min(K, k_begin + p.kt_per_split * BK);
+    const int nk = (k_end - k_begin + BK - 1) / BK;
+
+    typename RegTileFor<float, TM, TN>::type rt;
+    rt.zero();
+
+    auto load_tile = [&](int kt, int s) {
+        const int k0 = k_begin + kt * BK;
+        float* as = As + s * BM * LA;
+        float* bs = Bs + s * BK * BN;
+#pragma unroll
+        for (int it = 0; it < (CA + NT - 1) / NT; ++it) {
+            const int e = tid + it * NT;
+            if (CA % NT == 0 || e < CA) {
+                const int i = e / (BK / 4), c = e - i * (BK / 4);
+                const int gm = m0 + i, gk = k0 + 4 * c;
+                const bool ok = gm < p.M && gk < k_end;
+                cp_async<16>(as + i * LA + 4 * c, ok ? p.At + (i64)gm * p.lda + gk : p.At, ok);
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < (CB + NT - 1) / NT; ++it) {
+            const int e = tid + it * NT;
+            if (CB % NT == 0 || e < CB) {
+                const int k = e / (BN / 4), c = e - k * (BN / 4);
+                const int gk = k0 + k, gn = n0 + 4 * c;
+                const bool ok = gk < k_end && gn < p.N;
+                cp_async<16>(bs + k * BN + 4 * c, ok ? p.Bp + (i64)gk * p.ldb + gn : p.Bp, ok);
+            }
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) load_tile(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + STAGES - 1;
+            if (nt < nk) load_tile(nt, nt % STAGES);
+            cp_async_commit();
+        }
+        const int s = kt % STAGES;
+        const float* as = As + s * BM * LA;
+        const float* bs = Bs + s * BK * BN;
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += KV) {
+            float av[TM][KV];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+                const Vec<float, KV> v = *reinterpret_cast<const Vec<float, KV>*>(as + (i * TY + ty) * LA + k4);
+#pragma unroll
+                for (int e = 0; e < KV; ++e) av[i][e] = v.v[e];
+            }
+#pragma unroll
+            for (int kk = 0; kk < KV; ++kk) {
+                float a[TM], b[TN];
+#pragma unroll
+                for (int i = 0; i < TM; ++i) a[i] = av[i][kk];
+                load_frag<float, TN, WB>(b, bs + (k4 + kk) * BN, tx, TX);
+                rt.fma(a, b);
+            }
+        }
+    }
+    cp_async_wait<0>();
+    float acc[TM][TN];
+    rt.unpack(acc);
+
+    if (p.splits > 1 && p.cluster_red) {
+        // The splits slice-CTAs of this tile are one cluster (cluster dims
+        // 1 x splits).  Each parks its partial tile in its own shared memory;
+        // after a cluster barrier, CTA z sums its share of the tile's
+        // elements over the slices in order 0..splits-1 through DSMEM --
+        // the order of splitk_reduce_kernel, so the same bits, in one launch
+        // with no partial slabs in HBM.
+        __syncthreads();  // the stage ring is free: reuse it for the partial tile
+        float* part = As;  // [BM][BN]
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int r = i * TY + ty;
+#pragma unroll
+            for (int g = 0; g < TN / WB; ++g) {
+                Vec<float, WB> o;
+#pragma unroll
+                for (int e = 0; e < WB; ++e) o.v[e] = acc[i][g * WB + e];
+                *reinterpret_cast<Vec<float, WB>*>(part + r * BN + g * TX * WB + tx * WB) = o;
+            }
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        const int S = p.splits, z = blockIdx.y;
+        constexpr int Q = BM * BN / 4;  // float4 chunks of the tile
+        const int q0 = (int)((long long)Q * z / S), q1 = (int)((long long)Q * (z + 1) / S);
+        const uint32_t local = smem_addr(part);
+        for (int q = q0 + tid; q < q1; q += NT) {
+            float4 sum;
+            for (int src = 0; src < S; ++src) {
+                uint32_t remote;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + q * 16), "r"(src));
+                float4 v;
+                asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(remote));
+                if (src == 0) {
+                    sum = v;
+                } else {
+                    sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+                }
+            }
+            const int r = (q * 4) / BN, c = (q * 4) % BN;
+            const int gm = m0 + r;
+            if (gm < p.M && p.vec_out && n0 + c + 4 <= p.N) {
+                float4 o = make_float4(p.alpha * sum.x, p.alpha * sum.y, p.alpha * sum.z, p.alpha * sum.w);
+                if (p.use_c) {
+                    const float4 cc = *reinterpret_cast<const float4*>(p.C + (i64)gm * p.ldc + n0 + c);
+                    o = make_float4(fmadd(p.alpha, sum.x, p.beta * cc.x), fmadd(p.alpha, sum.y, p.beta * cc.y),
+                                    fmadd(p.alpha, sum.z, p.beta * cc.z), fmadd(p.alpha, sum.w, p.beta * cc.w));
+                }
+                *reinterpret_cast<float4*>(p.out + (i64)gm * p.ldo + n0 + c) = o;
+            } else if (gm < p.M) {
+                const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int gn = n0 + c + e;
+                    if (gn < p.N)
+                        p.out[(i64)gm * p.ldo + gn] =
+                            p.use_c ? fmadd(p.alpha, sv[e], p.beta * p.C[(i64)gm * p.ldc + gn]) : p.alpha * sv[e];
+                }
+            }
+        }
+        // no CTA may leave while a peer still reads its shared memory
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        return;
+    }
+
+    if (p.splits > 1) {  // raw partial sums into this slice's Mp x Np slab
+        float* slab = p.partial + (i64)blockIdx.y * p.Mp * p.Np;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int gm = m0 + i * TY + ty;
+#pragma unroll
+            for (int g = 0; g < TN / WB; ++g) {
+                const int gn = n0 + g * TX * WB + tx * WB;
+                Vec<float, WB> o;
+#pragma unroll
+                for (int e = 0; e < WB; ++e) o.v[e] = acc[i][g * WB + e];
+                *reinterpret_cast<Vec<float, WB>*>(slab + (i64)gm * p.Np + gn) = o;
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int gm = m0 + i * TY + ty;
+        if (gm >= p.M) continue;
+#pragma unroll
+        for (int g = 0; g < TN / WB; ++g) {
+            const int gn0 = n0 + g * TX * WB + tx * WB;
+            if (p.vec_out && gn0 + WB <= p.N) {  // whole vector in range: one store
+                Vec<float, WB> o;
+                if (p.use_c) {
+                    const Vec<float, WB> cc = *reinterpret_cast<const Vec<float, WB>*>(p.C + (i64)gm * p.ldc + gn0);
+#pragma unroll
+                    for (int e = 0; e < WB; ++e) o.v[e] = fmadd(p.alpha, acc[i][g * WB + e], p.beta * cc.v[e]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < WB; ++e) o.v[e] = p.alpha * acc[i][g * WB + e];
+                }
+                *reinterpret_cast<Vec<float, WB>*>(p.out + (i64)gm * p.ldo + gn0) = o;
+                continue;
+            }
+#pragma unroll
+            for (int e = 0; e < WB; ++e) {
+                const int gn = gn0 + e;
+                if (gn >= p.N) continue;
+                float v = p.alpha * acc[i][g * WB + e];
+                if (p.use_c) v = fmadd(p.alpha, acc[i][g * WB + e], p.beta * p.C[(i64)gm * p.ldc + gn]);
                 p.out[(i64)gm * p.ldo + gn] = v;
             }
         }

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdio>
 #include <string>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "registry.h"
@@ -75,6 +76,18 @@ int launch_direct(const GemmCall& c) {
     return cudaGetLastError() == cudaSuccess ? AG_OK : fail(c, AG_ERR_CUDA, "direct kernel launch failed");
 }
 
+// in-place core (split-K family) shared memory: A stage [bm][bk + 4], B stage [bk][bn]
+constexpr size_t inplace_stage_bytes(int bm, int bn, int bk) { return (size_t)(bm * (bk + 4) + bk * bn) * 4; }
+constexpr int inplace_stages(int bm, int bn, int bk) {
+    return 4 * inplace_stage_bytes(bm, bn, bk) <= 96 * 1024 ? 4 : (3 * inplace_stage_bytes(bm, bn, bk) <= 200 * 1024 ? 3 : 2);
+}
+// the ring also holds one partial tile (bm x bn fp32) for the cluster reduction
+constexpr size_t inplace_smem_bytes(int bm, int bn, int bk) {
+    return inplace_stages(bm, bn, bk) * inplace_stage_bytes(bm, bn, bk) > (size_t)bm * bn * 4
+               ? inplace_stages(bm, bn, bk) * inplace_stage_bytes(bm, bn, bk)
+               : (size_t)bm * bn * 4;
+}
+
 // [At | Bp | split-K partial slabs], each 256-byte aligned
 template <typename T>
 size_t indirect_workspace_bytes(i64 M, i64 N, i64 K, int bm, int bn, int bk, int splits = 1) {
@@ -97,6 +110,88 @@ inline int group_rows(i64 tiles_m, i64 bm, i64 Kp, size_t elem) {
     return (int)std::min<i64>(g, tiles_m);
 }
 
+// the split-K family's in-place path: in-place core over `splits` K slices
+// into the partial slabs, then the fixed-order reduction (same slices, same
+// order as the packed path, so the same bits)
+template <int BM, int BN, int BK, int TM, int TN>
+int launch_inplace(const GemmCall& c) {
+    constexpr int STAGES = inplace_stages(BM, BN, BK);
+    constexpr size_t smem = inplace_smem_bytes(BM, BN, BK);
+    static_assert(smem <= 227 * 1024, "in-place stage ring exceeds shared memory");
+    auto kernel = inplace_gemm_kernel<BM, BN, BK, TM, TN, STAGES>;
+    static std::atomic<size_t> granted{0};
+    if (ensure_smem(kernel, smem, granted) != cudaSuccess) return fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
+    const i64 M = c.M, N = c.N, K = c.K;
+    const i64 Mp = round_up(M, BM), Np = round_up(N, BN), Kp = round_up(K, BK);
+    if (Mp > 0x7fffffff || Np > 0x7fffffff || Kp > 0x7fffffff) return fail(c, AG_ERR_SHAPE, "dimension too large");
+    const int splits = c.splits > 1 ? c.splits : 1;
+    const size_t need = indirect_workspace_bytes<float>(M, N, K, BM, BN, BK, splits);
+    if (c.ws_bytes < need || (need && c.ws == nullptr))
+        return fail(c, AG_ERR_SHAPE, "workspace too small for the split-K partial slabs");
+    const i64 tiles_m = Mp / BM, tiles_n = Np / BN, ktiles = Kp / BK;
+    if (tiles_m * tiles_n > 0x7fffffffLL) return fail(c, AG_ERR_SHAPE, "too many tiles");
+    const int kps = (int)((ktiles + splits - 1) / splits);
+    const int used_splits = (int)((ktiles + kps - 1) / kps);
+    TiledParams<float> p;
+    p.Mp = (int)Mp; p.Np = (int)Np; p.Kp = (int)Kp; p.M = (int)M; p.N = (int)N;
+    p.alpha = (float)c.alpha; p.beta = (float)c.beta;
+    p.use_c = c.beta != 0.0;
+    // 16-byte vector stores (and C loads) when out / C rows allow them
+    p.vec_out = (c.ldo % 4 == 0) && aligned(c.out, 16) && (!p.use_c || ((c.ldc % 4 == 0) && aligned(c.C, 16)));
+    p.At = static_cast<const float*>(c.A); p.lda = c.lda;
+    p.Bp = static_cast<const float*>(c.B); p.ldb = c.ldb;
+    p.C = static_cast<const float*>(c.C); p.ldc = c.ldc;
+    p.out = static_cast<float*>(c.out); p.ldo = c.ldo;
+    p.bm = BM; p.bn = BN; p.bk = BK; p.uk = 1;
+    p.tiles_m = (int)tiles_m; p.tiles_n = (int)tiles_n; p.group_m = group_rows(tiles_m, BM, Kp, sizeof(float));
+    p.splits = used_splits; p.kt_per_split = kps;
+    p.partial = reinterpret_cast<float*>(static_cast<char*>(c.ws) + round_up(Kp * Mp * (i64)sizeof(float), 256) +
+                                         round_up(Kp * Np * (i64)sizeof(float), 256));
+    const dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)used_splits);
+    // one launch: the slices of a tile form a cluster and reduce over DSMEM
+    // (up to 16 slices: non-portable cluster sizes above 8); otherwise the
+    // slab + splitk_reduce_kernel path, same summation order
+    p.cluster_red = 0;
+    if (used_splits > 1 && used_splits <= 16 && tiles_m * tiles_n <= 65535) {
+        static std::atomic<int> np_ok{0};
+        if (used_splits > 8 && !np_ok.load()) {
+            if (cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
+                np_ok.store(1);
+            else
+                cudaGetLastError();
+        }
+        if (used_splits <= 8 || np_ok.load()) {
+            p.cluster_red = 1;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = grid;
+            cfg.blockDim = dim3((BM / TM) * (BN / TN));
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = c.stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 1;
+            attr[0].val.clusterDim.y = (unsigned)used_splits;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, kernel, p, (int)K) == cudaSuccess) return AG_OK;
+            cudaGetLastError();  // cluster shape not schedulable: fall back
+            p.cluster_red = 0;
+        }
+    }
+    kernel<<<grid, (BM / TM) * (BN / TN), smem, c.stream>>>(p, (int)K);
+    if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "in-place kernel launch failed");
+    if (used_splits > 1) {
+        const i64 total = M * N;
+        const unsigned blocks = (unsigned)std::min<i64>((total + 255) / 256, 148 * 16);
+        splitk_reduce_kernel<float><<<blocks, 256, 0, c.stream>>>(p.partial, used_splits, Mp * Np, (int)Np, (int)M,
+                                                                   (int)N, p.alpha, p.beta, p.use_c, p.C, c.ldc,
+                                                                   p.out, c.ldo);
+        if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "split-K reduce launch failed");
+    }
+    return AG_OK;
+}
+
 // AROW_OK (split-K family launchers): when op(A) is the caller's row-major
 // A and M, K are tile multiples, run the AROW core that reads A in place
 // instead of transpose-packing it.
@@ -114,6 +209,20 @@ int launch_indirect(const GemmCall& c) {
         return fail(c, AG_ERR_CONFIG, "config needs more threads per CTA than its kernel supports");
     if (bk % uk) return fail(c, AG_ERR_CONFIG, "block_k must be a multiple of unroll_k");
     const i64 M = c.M, N = c.N, K = c.K;
+    // split-K family, row-major operands with 16-byte rows: the in-place
+    // core streams both straight from the caller's layout (no packs).  For
+    // N > 64 with M, K tile multiples the AROW core (row-major A read in
+    // place by element copies, B packed) is kept: there the op(B) pack is
+    // small and the AROW core's main loop is the faster one (measured over
+    // the DeepBench / po2 sweeps); for narrow N its element copies of A are
+    // load-issue bound and the in-place core wins.
+    const bool arow_fit = !c.ta && M % bm == 0 && K % bk == 0;
+    const bool inplace = FIXED && AROW_OK && std::is_same<T, float>::value && !c.ta && !c.tb && K % 4 == 0 &&
+                         N % 4 == 0 && c.lda % 4 == 0 && c.ldb % 4 == 0 && aligned(c.A, 16) &&
+                         aligned(c.B, 16) && (N <= 64 || !arow_fit);
+    if constexpr (FIXED && AROW_OK && std::is_same<T, float>::value) {
+        if (inplace) return launch_inplace<BM, BN, BK, TM, TN>(c);
+    }
     const bool arow = FIXED && AROW_OK && !c.ta && M % bm == 0 && K % bk == 0;
     const size_t smem = arow ? tiled_smem_bytes<T>(bm + a_pad<T, true>(), bn, bk, STAGES_AROW)
                              : tiled_smem_bytes<T>(bm, bn, bk, STAGES);
@@ -184,7 +293,7 @@ int launch_indirect(const GemmCall& c) {
     p.out = static_cast<T*>(c.out); p.ldo = c.ldo;
     p.bm = bm; p.bn = bn; p.bk = bk; p.uk = uk;
     p.tiles_m = (int)tiles_m; p.tiles_n = (int)tiles_n; p.group_m = group_rows(tiles_m, bm, Kp, sizeof(T));
-    p.splits = used_splits; p.kt_per_split = kps;
+    p.splits = used_splits; p.kt_per_split = kps; p.cluster_red = 0;
     p.partial = reinterpret_cast<T*>(static_cast<char*>(c.ws) + round_up(Kp * Mp * (i64)sizeof(T), 256) +
                                      round_up(Kp * Np * (i64)sizeof(T), 256));
     const dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)used_splits);

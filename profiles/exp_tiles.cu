@@ -19,9 +19,19 @@ using namespace ag;
     X(128, 128, 16, 8, 16, 1)  \
     X(64, 256, 32, 8, 16, 1)
 
+// uk = 0 rows: the pack-free in-place core (split-K family's loader) with one
+// slice, i.e. the indirect family's math without the pack passes
+#define INPLACE_LIST(X)       \
+    X(128, 128, 32, 8, 8, 0)  \
+    X(64, 64, 16, 8, 8, 0)    \
+    X(128, 128, 32, 8, 16, 0) \
+    X(128, 256, 32, 8, 16, 0) \
+    X(128, 128, 32, 16, 8, 0)
+
 struct Exp { int bm, bn, bk, tm, tn, uk; LaunchFn fn; };
 #define EXP_ENTRY(bm, bn, bk, tm, tn, uk) {bm, bn, bk, tm, tn, uk, &launch_indirect<float, bm, bn, bk, tm, tn, uk>},
-static const Exp kExps[] = {EXP_LIST(EXP_ENTRY)};
+#define INPLACE_ENTRY(bm, bn, bk, tm, tn, uk) {bm, bn, bk, tm, tn, uk, &launch_inplace<bm, bn, bk, tm, tn>},
+static const Exp kExps[] = {EXP_LIST(EXP_ENTRY) INPLACE_LIST(INPLACE_ENTRY)};
 
 extern "C" int exp_count() { return (int)(sizeof(kExps) / sizeof(kExps[0])); }
 extern "C" void exp_tile(int i, int* t) {

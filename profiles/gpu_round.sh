@@ -17,4 +17,7 @@ timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --cloc
 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:tiled_gemm -c 1 -f -o $O/prof_top python profiles/profile_step.py --only ${TOP_SHAPE:-5124x9124x2560} \
     > $O/prof_top.out 2>&1
+# the tensor-core DT's dominant kernel (configs[4] roofline traffic)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 1 -c 1 -f -o $O/prof_tc \
+    python profiles/one_gemm.py ${TC_SHAPE:-7640x4746x6966} ${TC_CFG:-bf16:256-256-64-6-1-1} 2 > $O/prof_tc.out 2>&1
 echo done

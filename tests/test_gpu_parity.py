@@ -320,3 +320,40 @@ def test_splitk_row_major_a_path(canon):
     out2, _ = gemm_execute(s, cfg, A, B, C, B200)
     assert_rf(out1, ref)
     np.testing.assert_array_equal(out1, out2)
+
+
+SPLITK_ALL = [c for c in full_search_space(B200) if c.family is KernelFamily.SPLITK]
+
+
+@pytest.mark.parametrize("mnk", [(70, 36, 1000), (257, 100, 644), (35, 708, 2560), (1000, 16, 64)])
+def test_splitk_inplace_path_bit_identical_to_packed(mnk):
+    """Row-major A and B with K, N multiples of 4: the split-K family runs the
+    pack-free in-place core.  Storing A transposed (transA) forces the packed
+    core on the same products in the same order: the bits must agree."""
+    s = ProblemShape(*mnk, alpha=1.25, beta=0.5)
+    A, B, C = rand_operands(s, seed=mnk[0])
+    st = ProblemShape(*mnk, alpha=1.25, beta=0.5, transA=True)
+    At = np.ascontiguousarray(A.T)
+    ref = _oracle_ref(s, A, B, C)
+    for cfg in SPLITK_ALL[::3]:
+        out_inplace, _ = gemm_execute(s, cfg, A, B, C, B200)
+        out_packed, _ = gemm_execute(st, cfg, At, B, C, B200)
+        np.testing.assert_array_equal(out_inplace, out_packed, err_msg=cfg.canonical())
+        assert rel_frobenius(out_inplace, ref) <= 1e-5, cfg.canonical()
+
+
+def test_splitk_inplace_device_offsets_and_fallbacks():
+    """Sub-matrix views (leading dimension > K) stay in place; K % 4 != 0 or
+    an unaligned base falls back to the packed path with the same result."""
+    import torch
+    cfg = KernelConfig.from_canonical("splitk:64-64-16-8-4-8")
+    for (m, n, k), off in (((300, 64, 512), 0), ((300, 64, 510), 0), ((300, 64, 512), 1)):
+        s = ProblemShape(m, n, k)
+        A, B, C = rand_operands(s, seed=k + off)
+        big = torch.zeros((m, k + 8 + off), dtype=torch.float32, device="cuda")
+        big[:, off:off + k] = torch.from_numpy(A).cuda()
+        dA = big[:, off:off + k]
+        dB, dC = torch.from_numpy(B).cuda(), torch.from_numpy(C).cuda()
+        out, _ = gemm_execute(s, cfg, dA, dB, dC, B200)
+        want, _ = gemm_execute(ProblemShape(m, n, k, transA=True), cfg, np.ascontiguousarray(A.T), B, C, B200)
+        np.testing.assert_array_equal(out.cpu().numpy(), want)
