@@ -194,6 +194,9 @@ def pack_launches(shape, cfg) -> int:
         return 1
     if cfg.family in TC_FAMILIES:  # bf16: one convert pass per operand; tf32 reads fp32 in place
         return 3 if cfg.family is KernelFamily.BF16 else 1
+    if cfg.family is KernelFamily.TMA and not shape.transA and not shape.transB and shape.K % 4 == 0 \
+            and shape.N % 4 == 0:
+        return 1  # TMA-fed core on the caller's operands, no packs
     arow_fit = not shape.transA and shape.M % cfg.block_m == 0 and shape.K % cfg.block_k == 0
     if (cfg.family is KernelFamily.SPLITK and not shape.transA and not shape.transB and shape.K % 4 == 0
             and shape.N % 4 == 0 and (shape.N <= 64 or not arow_fit)):

@@ -53,6 +53,10 @@ extern "C" {
  * 64 bf16 elements), tm = shared-memory pipeline stages, tn = uk = 1. */
 #define AG_FAMILY_TF32 3
 #define AG_FAMILY_BF16 4
+/* B200 profiles: the indirect core's tiles fed by TMA from row-major
+ * operands (no pack passes; transposed / unaligned operands run the packed
+ * core with the same tile and the same bits) */
+#define AG_FAMILY_TMA 5
 
 /* element types accepted by gemm_execute (kernels.py:282-283) */
 #define AG_F32 0

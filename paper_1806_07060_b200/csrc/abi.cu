@@ -63,7 +63,7 @@ Registry& registry() {
 
 bool in_range(const ag_config& c) {
     return c.bm > 0 && c.bn > 0 && c.bk > 0 && c.tm > 0 && c.tn > 0 && c.uk > 0 && c.bm < 2048 && c.bn < 2048 &&
-           c.bk < 512 && c.tm < 64 && c.tn < 64 && c.uk < 64;
+           c.bk < 512 && c.tm < 64 && c.tn < 64 && c.uk <= 64;
 }
 
 // exact instantiation, else the run-time-tile kernel for (tm, tn) -- register
@@ -83,6 +83,12 @@ ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
         it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, 0, 0, 0, rtm, rtn, 0));
         return it != m.end() ? it->second : nullptr;
     }
+    if (c.family == AG_FAMILY_TMA) {  // float32: its own launcher; float64: the indirect run-time-tile kernel
+        auto it = m.find(make_key(AG_FAMILY_TMA, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk));
+        if (it != m.end()) return it->second;
+        it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, 0, 0, 0, rtm, rtn, 0));
+        return it != m.end() ? it->second : nullptr;
+    }
     auto it = m.find(make_key(c.family, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk));
     if (it != m.end()) return it->second;
     it = m.find(make_key(c.family, dtype, 0, 0, 0, c.tm, c.tn, 0));
@@ -98,6 +104,7 @@ std::string config_str(const ag_config& c) {
                       : c.family == AG_FAMILY_SPLITK ? "splitk"
                       : c.family == AG_FAMILY_TF32   ? "tf32"
                       : c.family == AG_FAMILY_BF16   ? "bf16"
+                      : c.family == AG_FAMILY_TMA    ? "tma"
                                                      : "indirect";
     snprintf(buf, sizeof buf, "%s:%d-%d-%d-%d-%d-%d", fam, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk);
     return buf;
@@ -376,12 +383,18 @@ int ag_is_legal(const ag_config* c, const ag_caps* caps) {
         const int64_t smem = (int64_t)c->tm * (128 + c->bn / ctas) * 128 + 1024 + (int64_t)ag::tc::EPI_BYTES + 256;
         return smem <= 227 * 1024;
     }
-    if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT && c->family != AG_FAMILY_SPLITK) return 0;
+    if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT && c->family != AG_FAMILY_SPLITK &&
+        c->family != AG_FAMILY_TMA)
+        return 0;
     if (c->family == AG_FAMILY_DIRECT && c->uk != 1) return 0;
+    if (c->family == AG_FAMILY_TMA) {  // spaces.is_legal_tuple: one 128-byte A row per k block, TMA boxes <= 256
+        if (c->bk != 32 || c->uk != 1 || c->bm > 256 || c->bn > 256 || c->bn % 4) return 0;
+        if (c->bm % c->tm || c->bn % c->tn || ((c->bm / c->tm) * (c->bn / c->tn)) % 32) return 0;
+    }
     if (c->family == AG_FAMILY_SPLITK) {
         if (c->uk < 2 || c->uk > 64) return 0;  // K slices
         if (c->bm % c->tm || c->bn % c->tn) return 0;
-    } else if (c->bm % c->tm || c->bn % c->tn || c->bk % c->uk) {
+    } else if (c->family != AG_FAMILY_TMA && (c->bm % c->tm || c->bn % c->tn || c->bk % c->uk)) {
         return 0;
     }
     const int64_t cap = c->family == AG_FAMILY_DIRECT ? caps->register_tile_cap_direct : caps->register_tile_cap_indirect;

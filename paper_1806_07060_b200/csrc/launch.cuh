@@ -152,7 +152,11 @@ int launch_inplace(const GemmCall& c) {
     // (up to 16 slices: non-portable cluster sizes above 8); otherwise the
     // slab + splitk_reduce_kernel path, same summation order
     p.cluster_red = 0;
-    if (used_splits > 1 && used_splits <= 16 && tiles_m * tiles_n <= 65535) {
+#ifdef AG_NO_CLUSTER_REDUCE  // measurement knob (profiles/exp_tiles.cu): slab + reduce kernel only
+    if (false) {
+#else
+    if (used_splits > 1 && used_splits <= 16) {
+#endif
         static std::atomic<int> np_ok{0};
         if (used_splits > 8 && !np_ok.load()) {
             if (cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)

@@ -43,6 +43,8 @@ class KernelFamily(str, Enum):
     profiles.  TF32 / BF16 are the tensor-core families (tcgen05.mma, TMEM
     accumulators, TMA): float32 operands packed to tf32 (round to nearest)
     or bf16, fp32 accumulation; they exist only in the "b200tc" profile.
+    TMA is the indirect core's fp32 arithmetic fed by TMA from the caller's
+    row-major operands (no pack passes; B200 profiles only).
     Reference-profile spaces, tables and dispatchers are unchanged.
     """
 
@@ -51,6 +53,7 @@ class KernelFamily(str, Enum):
     SPLITK = "splitk"
     TF32 = "tf32"
     BF16 = "bf16"
+    TMA = "tma"
 
 
 TC_FAMILIES = (KernelFamily.TF32, KernelFamily.BF16)
@@ -61,7 +64,8 @@ _FAMILY_CODE = {KernelFamily.DIRECT: _native.AG_FAMILY_DIRECT,
                 KernelFamily.INDIRECT: _native.AG_FAMILY_INDIRECT,
                 KernelFamily.SPLITK: _native.AG_FAMILY_SPLITK,
                 KernelFamily.TF32: _native.AG_FAMILY_TF32,
-                KernelFamily.BF16: _native.AG_FAMILY_BF16}
+                KernelFamily.BF16: _native.AG_FAMILY_BF16,
+                KernelFamily.TMA: _native.AG_FAMILY_TMA}
 _CODE_FAMILY = {v: k for k, v in _FAMILY_CODE.items()}
 
 
@@ -215,6 +219,13 @@ def domains_for(family: KernelFamily) -> dict[str, tuple[int, ...]]:
                 "tile_m": tuple(sorted({t[2] for t in spaces.SPLITK_TILES})),
                 "tile_n": tuple(sorted({t[3] for t in spaces.SPLITK_TILES})),
                 "unroll_k": spaces.SPLITK_SLICES}
+    if family is KernelFamily.TMA:
+        return {"block_m": tuple(sorted({t[0] for t in spaces.TMA_TILES})),
+                "block_n": tuple(sorted({t[1] for t in spaces.TMA_TILES})),
+                "block_k": (spaces.TMA_BLOCK_K,),
+                "tile_m": tuple(sorted({t[2] for t in spaces.TMA_TILES})),
+                "tile_n": tuple(sorted({t[3] for t in spaces.TMA_TILES})),
+                "unroll_k": (1,)}
     return DIRECT_DOMAINS if family is KernelFamily.DIRECT else INDIRECT_DOMAINS
 
 

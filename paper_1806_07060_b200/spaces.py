@@ -75,7 +75,15 @@ TC_BLOCK_N = (64, 128, 256)
 TC_BLOCK_K = {"tf32": 32, "bf16": 64}
 TC_STAGES = (2, 3, 4, 6)
 TC_SMEM_LIMIT = 227 * 1024
-FAMILIES = ("direct", "indirect", "splitk") + TC_FAMILIES
+# B200 profiles, TMA family ("tma"): the indirect core's tiles fed by TMA
+# straight from the caller's row-major A and B (csrc/fp32_tma.cuh): no pack
+# passes, mbarrier ring instead of cp.async + __syncthreads.  bk is one
+# 128-byte swizzle row (32 fp32); uk = 1.  Transposed or unaligned operands
+# run the same tile through the packed core (same bits).
+TMA_TILES = ((128, 128, 8, 8), (128, 64, 8, 8), (64, 128, 8, 8), (64, 64, 8, 8), (64, 64, 8, 4),
+             (64, 64, 4, 8), (64, 32, 8, 4), (32, 64, 4, 8))
+TMA_BLOCK_K = 32
+FAMILIES = ("direct", "indirect", "splitk") + TC_FAMILIES + ("tma",)
 
 PROFILE_REFERENCE = "reference"
 PROFILE_B200 = "b200"
@@ -134,12 +142,18 @@ def is_legal_tuple(family, bm, bn, bk, tm, tn, uk, caps) -> bool:
         return tc_smem_bytes(bm, bn, tm) <= TC_SMEM_LIMIT
     if family == "direct" and uk != 1:
         return False
+    if family == "tma":
+        # one 128-byte A row per k block, boxes of at most 256 rows, whole warps
+        if bk != TMA_BLOCK_K or uk != 1 or bm > 256 or bn > 256 or bn % 4:
+            return False
+        if bm % tm or bn % tn or ((bm // tm) * (bn // tn)) % 32:
+            return False
     if family == "splitk":
         if not 2 <= uk <= 64:  # uk carries the number of K slices
             return False
         if bm % tm or bn % tn:
             return False
-    elif bm % tm or bn % tn or bk % uk:
+    elif family != "tma" and (bm % tm or bn % tn or bk % uk):
         return False
     cap = caps["register_tile_cap_direct"] if family == "direct" else caps["register_tile_cap_indirect"]
     if tm * tn > cap:
@@ -166,6 +180,11 @@ def enumerate_tuples(family, caps, profile=PROFILE_REFERENCE):
             return []
         return [t for bm in TC_BLOCK_M for bn in TC_BLOCK_N for st in TC_STAGES
                 for t in [(family, bm, bn, TC_BLOCK_K[family], st, 1, 1)] if is_legal_tuple(*t, caps)]
+    if family == "tma":
+        if not is_b200_profile(profile):
+            return []
+        return [t for (bm, bn, tm, tn) in TMA_TILES
+                for t in [("tma", bm, bn, TMA_BLOCK_K, tm, tn, 1)] if is_legal_tuple(*t, caps)]
     if family == "splitk":
         if not is_b200_profile(profile):
             return []

@@ -23,15 +23,18 @@ def lib():
                                str(HERE / "exp_tiles.cu")])
     L = ctypes.CDLL(str(so))
     L.exp_ws.restype = ctypes.c_size_t
-    L.exp_ws.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
+    L.exp_ws.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]
     L.exp_time.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
-                           ctypes.POINTER(ctypes.c_double)]
+                           ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     return L
 
 
 def main():
+    import os
     import torch
+    if os.environ.get("EXP_SKINNY"):
+        return skinny(torch)
     L = lib()
     n = L.exp_count()
     tiles = []
@@ -46,11 +49,11 @@ def main():
         ref = None
         res = {}
         for i in range(n):
-            ws_n = L.exp_ws(i, m, nn, k)
+            ws_n = L.exp_ws(i, m, nn, k, 1)
             ws = torch.empty(ws_n, dtype=torch.uint8, device="cuda")
             sec = ctypes.c_double()
             rc = L.exp_time(i, m, nn, k, a.data_ptr(), b.data_ptr(), out.data_ptr(), ws.data_ptr(), ws_n, 5,
-                            ctypes.byref(sec))
+                            1, ctypes.byref(sec))
             if rc:
                 res[tiles[i]] = f"rc={rc}"
                 continue
@@ -64,6 +67,41 @@ def main():
         print(json.dumps({"mnk": [m, nn, k], "tflops": res}), flush=True)
         del a, b, out, ref
         torch.cuda.empty_cache()
+
+
+SKINNY = [(4096, 16, 4096), (2048, 16, 2048), (7680, 16, 2560), (1760, 16, 1760), (3072, 16, 1024),
+          (4096, 32, 4096), (1760, 32, 1760), (7680, 32, 2560)]
+
+
+def skinny(torch):
+    """In-place split-K candidates (uk = 0 rows) on N <= 32 shapes, slices 2..32."""
+    L = lib()
+    n = L.exp_count()
+    tiles = []
+    for i in range(n):
+        t = (ctypes.c_int * 6)()
+        L.exp_tile(i, t)
+        tiles.append(tuple(t))
+    for (m, nn, k) in SKINNY:
+        a = torch.rand(m, k, device="cuda") - 0.5
+        b = torch.rand(k, nn, device="cuda") - 0.5
+        out = torch.empty(m, nn, device="cuda")
+        res = {}
+        for i, t in enumerate(tiles):
+            if t[5] != 0 or t[1] > nn:
+                continue
+            best = None
+            for splits in (2, 4, 8, 16):
+                ws_n = L.exp_ws(i, m, nn, k, splits)
+                ws = torch.empty(ws_n, dtype=torch.uint8, device="cuda")
+                sec = ctypes.c_double()
+                rc = L.exp_time(i, m, nn, k, a.data_ptr(), b.data_ptr(), out.data_ptr(), ws.data_ptr(), ws_n, 7,
+                                splits, ctypes.byref(sec))
+                if rc == 0 and (best is None or sec.value < best[0]):
+                    best = (sec.value, splits)
+            if best:
+                res["-".join(map(str, t[:5]))] = [round(2 * m * nn * k / best[0] / 1e12, 2), best[1]]
+        print(json.dumps({"mnk": [m, nn, k], "tflops_slices": res}), flush=True)
 
 
 if __name__ == "__main__":

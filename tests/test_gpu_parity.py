@@ -357,3 +357,52 @@ def test_splitk_inplace_device_offsets_and_fallbacks():
         out, _ = gemm_execute(s, cfg, dA, dB, dC, B200)
         want, _ = gemm_execute(ProblemShape(m, n, k, transA=True), cfg, np.ascontiguousarray(A.T), B, C, B200)
         np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("slices", [3, 16, 32, 64])
+def test_splitk_inplace_cluster_and_slab_reductions(slices):
+    """Up to 16 slices reduce inside a thread-block cluster over DSMEM; more
+    (legal up to 64) take the partial-slab + reduction-kernel path.  Both sum
+    the slices in order, so the packed (transA) path gives the same bits."""
+    cfg = KernelConfig(KernelFamily.SPLITK, 32, 32, 16, 4, 4, slices)
+    s = ProblemShape(100, 68, 2048, alpha=1.5, beta=0.25)
+    A, B, C = rand_operands(s, seed=slices)
+    out, _ = gemm_execute(s, cfg, A, B, C, B200)
+    st = ProblemShape(100, 68, 2048, alpha=1.5, beta=0.25, transA=True)
+    want, _ = gemm_execute(st, cfg, np.ascontiguousarray(A.T), B, C, B200)
+    np.testing.assert_array_equal(out, want)
+    assert_rf(out, _oracle_ref(s, A, B, C))
+
+
+TMA_ALL = [c for c in full_search_space(B200) if c.family is KernelFamily.TMA]
+
+
+@pytest.mark.parametrize("mnk,beta", [((300, 260, 516), 0.0), ((129, 68, 36), 0.5), ((1000, 1000, 1000), 0.0),
+                                      ((77, 1024, 4), 1.0)])
+def test_tma_family_bit_identical_to_packed_core(mnk, beta):
+    """The TMA-fed core (row-major operands, zero fill by the TMA unit) and the
+    packed indirect core with the same tile compute the same FMA sequence."""
+    s = ProblemShape(*mnk, alpha=1.25, beta=beta)
+    A, B, C = rand_operands(s, seed=sum(mnk))
+    ref = _oracle_ref(s, A, B, C)
+    assert len(TMA_ALL) == 8
+    for cfg in TMA_ALL:
+        packed = KernelConfig(KernelFamily.INDIRECT, cfg.block_m, cfg.block_n, 32, cfg.tile_m, cfg.tile_n, 1)
+        out_tma, _ = gemm_execute(s, cfg, A, B, C, B200)
+        out_packed, _ = gemm_execute(s, packed, A, B, C, B200)
+        np.testing.assert_array_equal(out_tma, out_packed, err_msg=cfg.canonical())
+        assert rel_frobenius(out_tma, ref) <= 1e-5
+
+
+def test_tma_family_fallbacks():
+    """Transposed operands, K % 4 != 0 and float64 run the packed path."""
+    cfg = KernelConfig.from_canonical("tma:64-64-32-8-8-1")
+    for s in (ProblemShape(90, 70, 50, transA=True, beta=0.5), ProblemShape(90, 70, 50, transB=True),
+              ProblemShape(90, 70, 51)):
+        A, B, C = rand_operands(s, seed=5)
+        out, _ = gemm_execute(s, cfg, A, B, C, B200)
+        assert_rf(out, _oracle_ref(s, A, B, C))
+    s = ProblemShape(90, 70, 52, beta=0.5)
+    A, B, C = rand_operands(s, np.float64, seed=6)
+    out, _ = gemm_execute(s, cfg, A, B, C, B200)
+    assert out.dtype == np.float64 and rel_frobenius(out, _oracle_ref(s, A, B, C)) <= 1e-12

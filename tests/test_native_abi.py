@@ -63,7 +63,7 @@ def test_native_legality_equals_python(caps):
     lib = _native.lib()
     ncaps = caps.native()
     grid = [(f, bm, bn, bk, tm, tn, uk)
-            for f in (KernelFamily.DIRECT, KernelFamily.INDIRECT, KernelFamily.SPLITK)
+            for f in (KernelFamily.DIRECT, KernelFamily.INDIRECT, KernelFamily.SPLITK, KernelFamily.TMA)
             for bm in (8, 16, 24, 64, 256) for bn in (8, 32, 128) for bk in (8, 16, 32)
             for tm in (1, 2, 3, 8) for tn in (1, 4, 8) for uk in (1, 2)]
     for t in grid:
