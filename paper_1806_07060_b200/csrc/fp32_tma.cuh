@@ -53,7 +53,9 @@ tma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     static_assert(NT % 32 == 0, "whole warps");
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    // 1024-byte aligned (128-byte swizzle atoms); offset from the shared-window
+    // address so the pointer stays in the shared space (LDS/STS, not generic)
+    uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;                     // [STAGES][BM][128 B], 128-byte swizzle
     uint8_t* sB = smem + STAGES * A_BYTES;  // [STAGES][BK][BN] fp32
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);

@@ -273,7 +273,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     static_assert(BNC % CH == 0 || CTAS == 1, "pair tiles split B into whole 128-byte chunks");
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    // 1024-byte aligned (128-byte swizzle atoms); offset from the shared-window
+    // address so the pointer stays in the shared space (LDS/STS, not generic)
+    uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
     float* sEpi = reinterpret_cast<float*>(sB + STAGES * B_BYTES);

@@ -19,15 +19,19 @@ def init(backend: str | None = None):
     import torch.distributed as dist
 
     rank, world, local = env_rank_world()
+    ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # AG_DIST_BACKEND=gloo lets several ranks share one GPU (a functional
+        # check of the N > 1 path on a 1-GPU box; NCCL refuses duplicate GPUs)
+        backend = backend or os.environ.get("AG_DIST_BACKEND") or ("nccl" if ndev else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
+        elif ndev:
+            torch.cuda.set_device(local % ndev)
         dist.init_process_group(backend=backend, rank=rank, world_size=world)
-    elif torch.cuda.is_available():
-        torch.cuda.set_device(local)
+    elif ndev:
+        torch.cuda.set_device(local % ndev)
     return rank, world, local
 
 
@@ -43,6 +47,8 @@ def reduce_max(values: list, device=None) -> list:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return list(values)
+    if dist.get_backend() != "nccl":
+        device = None  # gloo reduces host tensors
     t = torch.tensor(values, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()
