@@ -274,7 +274,12 @@ def clocks_sampler():
     fields = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-    idx = os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[int(os.environ.get("LOCAL_RANK", "0"))]
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = max(1, torch.cuda.device_count())
+    local = local if local < ndev else 0  # ranks sharing one GPU (AG_DIST_BACKEND=gloo)
+    visible = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    idx = visible[local] if local < len(visible) else str(local)
     out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
     try:
         proc = subprocess.Popen(["nvidia-smi", f"--id={idx}", f"--query-gpu={fields}", "--format=csv,noheader,nounits",
@@ -322,6 +327,7 @@ def cpu_rates(shapes, budget_flops=CPU_SAMPLE_FLOPS):
     from oracle import gemm as ogemm
     from paper_1806_07060_b200.tuner import _bench_buffers
     ogemm.build()
+    ogemm.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
     rates = []
     for s in shapes:
         canon = CPU_DEFAULT_DIRECT if s.M * s.N * s.K < 384 ** 3 else CPU_DEFAULT_INDIRECT
@@ -520,7 +526,7 @@ def run_ours(args):
 
     # ---- CPU baseline (oracle port) on rank 0, bounded sample
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # rank 0 at N = 1 only
         t0 = time.perf_counter()
         cpu_r, cores = cpu_rates(workload)
         cpu = {"value": round(geomean(cpu_r), 4), "unit": "GFLOP/s", "cores": cores, "kind": "port",

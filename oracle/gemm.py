@@ -41,6 +41,8 @@ def lib():
         h.oracle_pack.argtypes = [_int, _p, _i64, _i64, _i64, _int, _p, _i64, _i64]
         h.oracle_pack.restype = None
         h.oracle_num_threads.restype = _int
+        h.oracle_set_threads.argtypes = [_int]
+        h.oracle_set_threads.restype = None
         _lib = h
     return _lib
 
@@ -92,3 +94,7 @@ def pack_padded(X, rows, cols, transpose, pad_rows, pad_cols):
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(int(n))

@@ -187,3 +187,14 @@ int oracle_num_threads(void) {
     return 1;
 #endif
 }
+
+/* the CPU baseline uses every host thread, whatever OMP_NUM_THREADS a
+   launcher (torchrun sets 1) left in the environment */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
