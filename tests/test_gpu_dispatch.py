@@ -135,6 +135,8 @@ HOST_CASES = [
     (1000, 64, 1024, 1.0, 0.0, False, False, "splitk:64-64-16-8-4-8"),    # split-K
     (600, 520, 300, 1.0, 0.25, False, False, "bf16:256-128-64-4-1-1"),    # tensor-core pair
     (260, 650, 96, 1.0, 0.0, False, True, "tf32:128-64-32-4-1-1"),
+    (700, 300, 128, 1.0, 0.5, False, False, "tma:64-64-32-8-8-1"),        # TMA core, row panels
+    (300, 700, 128, 1.0, 0.0, False, False, "tma:128-128-32-8-8-1"),      # TMA core, column panels
 ]
 
 
