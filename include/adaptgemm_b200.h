@@ -123,7 +123,7 @@ int ag_gemm(const ag_shape* shape, const ag_config* config, const ag_caps* caps,
  * it), the family path, D2H of out.  The result is cut into `panels` row
  * panels (M >= N) or column panels (M < N), pipelined over three streams so
  * the PCIe copies of one panel overlap the kernels of the next; panels <= 0
- * picks 4 when the call moves >= 32 MB, else 1.  Each panel runs `config`
+ * picks 8 when the call moves >= 96 MB, 4 from 32 MB, else 1.  Each panel runs `config`
  * on a sub-problem with the same rows / columns and K order, so the result
  * equals ag_gemm's.  Host buffers should be pinned (pageable memory works
  * but its copies do not overlap).  `device_scratch` holds the staged

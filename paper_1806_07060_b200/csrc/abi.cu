@@ -325,9 +325,10 @@ bool plan_host(const ag_shape* s, const ag_config* c, int dtype, int panels, Hos
     h->elem = dtype == AG_F64 ? 8 : 4;
     h->by_rows = s->m >= s->n;
     h->extent = h->by_rows ? s->m : s->n;
-    // auto: ~4 panels once the call moves >= 32 MB, never panels under 256
+    // auto: 4 panels once the call moves >= 32 MB, 8 from 96 MB (measured,
+    // profiles/r01_e2e_probe.jsonl), never panels under 256
     const int64_t bytes = (s->m * s->k + s->k * s->n + 2 * s->m * s->n) * h->elem;
-    int p = panels > 0 ? panels : (bytes >= (32LL << 20) ? 4 : 1);
+    int p = panels > 0 ? panels : (bytes >= (96LL << 20) ? 8 : bytes >= (32LL << 20) ? 4 : 1);
     int64_t chunk = align_up((h->extent + p - 1) / p, 256);
     if (chunk >= h->extent) chunk = h->extent;
     h->chunk = chunk;
