@@ -45,6 +45,7 @@ DATA = ROOT / "paper_1806_07060_b200" / "data"
 PO2_BUNDLE = DATA / "tables_b200_po2.csv.gz"
 DB_BUNDLE = DATA / "tables_b200_deepbench.csv.gz"
 TC_BUNDLE = DATA / "tables_b200tc_random.csv.gz"
+GO2_BUNDLE = DATA / "tables_b200_go2.csv.gz"
 TRAFFIC_FILE = ROOT / "profiles" / "roofline_traffic.json"
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -150,6 +151,51 @@ def build_tc_model(policy):
             "test": [ProblemShapeOf(recs[i][0]) for i in sp.test], "fixed_tc": fixed, "n_train": len(train_recs),
             "score": {"accuracy": best.accuracy, "dtpr": best.dtpr, "dttr": best.dttr,
                       "leaves": best.stats.total_leaves, "height": best.stats.height}}
+
+
+def go2_section():
+    """The paper's dense dataset (go2: 256..3840 step 256, 3375 shapes) on
+    B200 tables (configs/go2_b200.json: the 133-config fp32 shortlist), run
+    through the reference pipeline in table mode: seeded 80/20 split, the
+    5 x 8 CART grid, selection by test DTPR; reports the reference's metrics
+    (accuracy, DTPR, DTTR) and the table-mode geomeans (no GPU time)."""
+    from paper_1806_07060_b200 import evaluation, model
+    from paper_1806_07060_b200.dataset import dataset_from_tables, split
+    from paper_1806_07060_b200.tuner import load_table_bundle
+
+    if not GO2_BUNDLE.exists():
+        return {"unavailable": f"no {GO2_BUNDLE.name}"}
+    tables = load_table_bundle(GO2_BUNDLE)
+    ds = dataset_from_tables(tables, "go2")
+    sp = split(ds, SPLIT_FRACTION, SPLIT_SEED)
+    recs = ds.features_and_labels()
+    train_recs = [recs[i] for i in sp.train]
+    test_recs = [recs[i] for i in sp.test]
+    t0 = time.perf_counter()
+    named = model.grid_train(train_recs)
+    train_s = time.perf_counter() - t0
+    by_shape = evaluation.tables_by_shape(tables)
+    policy = evaluation.build_baseline_policy(by_shape[(256, 256, 256)], by_shape[(1024, 1024, 1024)],
+                                              384).register(ds.class_index)
+    scores = evaluation.score_models(named, test_recs, by_shape, ds.class_index, policy)
+    best = evaluation.select_best_model(scores)
+    tree = dict(named)[best.name]
+    dt, orc, de = [], [], []
+    for mnk, _ in test_recs:
+        t = by_shape[mnk]
+        cid = model.predict(tree, mnk)
+        cfg = ds.class_index.config_of(cid)
+        dt.append(t.gflops_for(cfg))
+        orc.append(t.peak_gflops)
+        de.append(t.gflops_for(policy.select_config(ProblemShapeOf(mnk))))
+    return {"shapes": len(tables), "configs_per_shape": len(tables[0].measurements), "n_train": len(train_recs),
+            "n_test": len(test_recs), "model": best.name,
+            "accuracy": round(best.accuracy, 4), "dtpr": round(best.dtpr, 4), "dttr": round(best.dttr, 4),
+            "leaves": best.stats.total_leaves, "height": best.stats.height,
+            "grid_train_s": round(train_s, 2),
+            "dt_geomean_table": round(geomean(dt), 1), "oracle_geomean_table": round(geomean(orc), 1),
+            "default_geomean_table": round(geomean(de), 1),
+            "paper_p100_go2_hmax_l1": {"accuracy": 0.60, "dtpr": 0.852, "dttr": 1.424}}
 
 
 def ProblemShapeOf(mnk):
@@ -484,6 +530,7 @@ def run_ours(args):
 
     # ---- configs[4]: the tensor-core search space on random (M, N, K)
     tc_doc = tc_section(m, policy, device, distributed, times, fallback, args)
+    go2_doc = go2_section() if rank == 0 else None
     # ---- configs[3]: sharded exhaustive sweep throughput
     sweep_doc = sweep_section(device, distributed, rank, world) if not args.no_sweep else None
 
@@ -580,6 +627,7 @@ def run_ours(args):
                      "note": "event time covers the whole family path (pack helpers + tiled core)"},
         "cpu_baseline": cpu,
         "tc_random": tc_doc,
+        "go2_table_mode": go2_doc,
         "sweep": sweep_doc,
         "clocks": clocks,
         "gpu_launches": launches,
