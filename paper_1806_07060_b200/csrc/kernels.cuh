@@ -822,6 +822,45 @@ pack_pad_kernel(T* __restrict__ dst, i64 ld_dst, int dst_rows, int dst_cols,
     }
 }
 
+// Non-transposing pack (dst = zero-padded copy of src): a flat grid-stride
+// over the destination's 4-element quads, 4 quads per thread per step so 4
+// loads are in flight; destination stores are 16-byte vectors (the packed
+// buffers' rows are 16-byte multiples), source loads are vectors when the
+// source rows allow it.  Replaces the 32 x 32 tile path for this case:
+// 2048 x 8457 -> 2048 x 8576 went from 44.7 us (3.1 TB/s) to the copy rate.
+template <typename T, bool SRC_VEC>
+__global__ void __launch_bounds__(256)
+pack_copy_kernel(T* __restrict__ dst, i64 ld_dst, int dst_rows, int dst_cols, const T* __restrict__ src,
+                 i64 ld_src, int rows, int cols) {
+    constexpr int W = VecW<T>::W;  // elements per 16 bytes
+    const i64 qpr = dst_cols / W;
+    const i64 total = (i64)dst_rows * qpr;
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    for (i64 q0 = (i64)blockIdx.x * blockDim.x + threadIdx.x; q0 < total; q0 += 4 * stride) {
+        Vec<T, W> v[4];
+        i64 r[4], c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const i64 q = q0 + u * stride;
+            r[u] = q / qpr;
+            c[u] = (q - r[u] * qpr) * W;
+            if (q >= total) continue;
+            const T* sp = src + r[u] * ld_src + c[u];
+            if (SRC_VEC && r[u] < rows && c[u] + W <= cols) {
+                v[u] = *reinterpret_cast<const Vec<T, W>*>(sp);
+            } else {
+#pragma unroll
+                for (int e = 0; e < W; ++e) v[u].v[e] = (r[u] < rows && c[u] + e < cols) ? __ldg(sp + e) : T(0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (q0 + u * stride >= total) break;
+            *reinterpret_cast<Vec<T, W>*>(dst + r[u] * ld_dst + c[u]) = v[u];
+        }
+    }
+}
+
 // Textbook (i, j, k) GEMM with float64 accumulation: every multiply and add
 // separately rounded (no FMA contraction), k ascending, then
 // alpha*acc + beta*C in float64 rounded once to T -- the same operation

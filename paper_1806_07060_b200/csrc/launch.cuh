@@ -43,6 +43,25 @@ inline int fail(const GemmCall& c, int code, const std::string& msg) {
 template <typename T>
 int launch_pack(T* dst, i64 ld_dst, i64 dst_rows, i64 dst_cols, const T* src, i64 ld_src,
                 i64 rows, i64 cols, int transpose, cudaStream_t stream) {
+    constexpr int W = VecW<T>::W;
+    if (!transpose && dst_cols % W == 0 && ld_dst % W == 0 && aligned(dst, 16)) {
+        const bool vec = ld_src % W == 0 && aligned(src, 16);
+        const i64 total = dst_rows * (dst_cols / W);
+        static const int sms = [] {
+            int dev = 0, n = 148;
+            cudaGetDevice(&dev);
+            if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+            return n;
+        }();  // grid sizing only
+        const unsigned blocks = (unsigned)std::max<i64>(1, std::min<i64>((total + 1023) / 1024, (i64)sms * 8));
+        if (vec)
+            pack_copy_kernel<T, true><<<blocks, 256, 0, stream>>>(dst, ld_dst, (int)dst_rows, (int)dst_cols, src,
+                                                                  ld_src, (int)rows, (int)cols);
+        else
+            pack_copy_kernel<T, false><<<blocks, 256, 0, stream>>>(dst, ld_dst, (int)dst_rows, (int)dst_cols, src,
+                                                                   ld_src, (int)rows, (int)cols);
+        return cudaGetLastError() == cudaSuccess ? AG_OK : AG_ERR_CUDA;
+    }
     dim3 grid((unsigned)((dst_cols + 31) / 32), (unsigned)((dst_rows + 31) / 32));
     if (grid.y > 65535u) return AG_ERR_SHAPE;
     pack_pad_kernel<T><<<grid, dim3(32, 8), 0, stream>>>(dst, ld_dst, (int)dst_rows, (int)dst_cols, src, ld_src,
