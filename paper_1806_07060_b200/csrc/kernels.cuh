@@ -545,15 +545,12 @@ tiled_gemm_kernel(const TiledParams<T> p) {
 // slice's K end (K and N multiples of 4, 16-byte aligned rows; the launcher
 // checks).  The A stage is row-major in shared memory ([BM][BK + 4], rows
 // 16-byte aligned, an odd number of 16-byte chunks apart so a warp's
-// LDS.128 / LDS.64 over consecutive rows is conflict free); each thread
-// reads 4 (or 2) k of a row with one load and applies them in k order, so every output
+// LDS.128 over consecutive rows is conflict free); each thread reads 4 k
+// of a row with one LDS.128 and applies them in k order, so every output
 // element sees exactly the FMA sequence of the packed core: the zero fill is
 // the pack's zero padding, and the result is bit-identical to it.  Thread
 // rows are strided by TY (row r = i * TY + ty), B columns interleaved as in
 // the packed core.
-#ifndef INPLACE_KV
-#define INPLACE_KV 4
-#endif
 template <int BM, int BN, int BK, int TM, int TN, int STAGES>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), ((BM / TM) * (BN / TN) >= 256 && TM * TN <= 64) ? 2 : 1)
 inplace_gemm_kernel(const TiledParams<float> p, int K) {
@@ -562,10 +559,9 @@ inplace_gemm_kernel(const TiledParams<float> p, int K) {
     constexpr int LA = BK + 4;  // A stage row stride (floats): 16-byte aligned, odd in chunks when BK % 8 == 0
     constexpr int WB = FragW<float, TN>::W;
     constexpr int CA = BM * (BK / 4), CB = BK * (BN / 4);
-    // k values per A fragment load: LDS.128 (4 k) for short register tiles,
-    // LDS.64 (2 k) for TM >= 8, which keeps the 8 x 8 tile at <= 128
-    // registers (two 256-thread CTAs per SM)
-    constexpr int KV = INPLACE_KV;
+    // k values per A fragment load: one LDS.128 per row per 4 k (2-k LDS.64
+    // loads measured the same; the 8 x 8 tile fits 128 registers either way)
+    constexpr int KV = 4;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* As = reinterpret_cast<float*>(smem_raw);  // [STAGES][BM][LA]
