@@ -529,8 +529,15 @@ def run_ours(args):
     po2_de = measured(po2_cases, [policy.select_config(c.shape) for c in po2_cases])
 
     # ---- configs[4]: the tensor-core search space on random (M, N, K)
-    tc_doc = tc_section(m, policy, device, distributed, times, fallback, args)
-    go2_doc = go2_section() if rank == 0 else None
+    # sub-measurements never take the headline line down with them
+    try:
+        tc_doc = tc_section(m, policy, device, distributed, times, fallback, args)
+    except Exception as exc:  # noqa: BLE001
+        tc_doc = {"error": f"{type(exc).__name__}: {exc}"}
+    try:
+        go2_doc = go2_section() if rank == 0 else None
+    except Exception as exc:  # noqa: BLE001
+        go2_doc = {"error": f"{type(exc).__name__}: {exc}"}
     # ---- configs[3]: sharded exhaustive sweep throughput
     sweep_doc = sweep_section(device, distributed, rank, world) if not args.no_sweep else None
 

@@ -1,6 +1,7 @@
 """Re-time one kernel family over a finished sweep and merge it in.
 
     python configs/resweep_family.py FAMILY CONFIG.json OLD_TABLES_DIR NEW_TABLES_DIR
+    python configs/resweep_family.py list:CFG1,CFG2 CONFIG.json OLD NEW   (explicit configs)
 
 For every shape of CONFIG: time the family's configs of the config's search
 space (list mode: the listed ones of that family) with the config's timing
@@ -31,11 +32,15 @@ def main():
     ap.add_argument("old")
     ap.add_argument("new")
     a = ap.parse_args()
-    fam = KernelFamily(a.family)
     cfg = cli.PipelineConfig.load(a.config)
     shapes, _ = cfg.shapes()
     order = full_order(cfg) or full_search_space(cfg.caps)
-    mine = [c for c in order if c.family is fam]
+    if a.family.startswith("list:"):  # explicit configs (e.g. a new default tile)
+        from paper_1806_07060_b200.kernels import KernelConfig
+        mine = [KernelConfig.from_canonical(x) for x in a.family[5:].split(",")]
+    else:
+        fam = KernelFamily(a.family)
+        mine = [c for c in order if c.family is fam]
     out = Path(a.new)
     out.mkdir(parents=True, exist_ok=True)
     for i, s in enumerate(shapes):
