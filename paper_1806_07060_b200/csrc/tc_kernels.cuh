@@ -548,43 +548,53 @@ __device__ __forceinline__ void store4(__nv_bfloat16* d, float a, float b, float
 __device__ __forceinline__ void store1(float* d, float a) { *d = a; }
 __device__ __forceinline__ void store1(__nv_bfloat16* d, float a) { *d = __float2bfloat16_rn(a); }
 
-// Flat grid-stride over the (row, 4-column quad) space, 4 quads per thread
-// per step so 4 loads are in flight (the row-per-block version reached
-// 5.3 TB/s on 7640 x 6966; this one streams at the copy rate).  SRC_VEC:
-// 16-byte source rows (one LDG.128 per quad), else 4 scalar loads.
-template <typename D, bool SRC_VEC>
+// One staging job: dst (rows x cols, ld_dst) = src converted to the MMA type.
+template <typename D>
+struct ConvertJob {
+    D* dst;
+    i64 ld_dst;
+    const float* src;
+    i64 ld_src;
+    i64 rows, cols, quads;  // quads = rows * ceil(cols / 4); 0 = no job
+    int vec;                // 16-byte source rows: one LDG.128 per quad
+};
+
+// Both operands' staging in ONE launch: a flat grid-stride over the
+// (row, 4-column quad) space of job a then job b, 4 quads per thread per step
+// so 4 loads are in flight.  (Separate row-per-block launches reached
+// 5.3 TB/s on 7640 x 6966; one flat launch streams at the copy rate and
+// pays one launch and one tail instead of two.)
+template <typename D>
+__device__ __forceinline__ void convert_quad(const ConvertJob<D>& j, i64 q) {
+    const i64 qpr = (j.cols + 3) >> 2;
+    const i64 r = q / qpr, c = (q - r * qpr) << 2;
+    const float* sp = j.src + r * j.ld_src + c;
+    D* dp = j.dst + r * j.ld_dst + c;
+    if (c + 4 <= j.cols) {
+        float4 v;
+        if (j.vec) {
+            v = __ldcs(reinterpret_cast<const float4*>(sp));
+        } else {
+            v = make_float4(__ldcs(sp), __ldcs(sp + 1), __ldcs(sp + 2), __ldcs(sp + 3));
+        }
+        store4(dp, v.x, v.y, v.z, v.w, true);
+    } else {
+        for (i64 k = c; k < j.cols; ++k) store1(j.dst + r * j.ld_dst + k, j.src[r * j.ld_src + k]);
+    }
+}
+template <typename D>
 __global__ void __launch_bounds__(256)
-tc_convert_kernel(D* __restrict__ dst, i64 ld_dst, const float* __restrict__ src, i64 ld_src, int rows, int cols) {
-    const i64 qpr = (cols + 3) >> 2;
-    const i64 total = (i64)rows * qpr;
+tc_convert_kernel(const ConvertJob<D> a, const ConvertJob<D> b) {
+    const i64 total = a.quads + b.quads;
     const i64 stride = (i64)gridDim.x * blockDim.x;
     for (i64 q0 = (i64)blockIdx.x * blockDim.x + threadIdx.x; q0 < total; q0 += 4 * stride) {
-        float4 v[4];
-        i64 r[4], c[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const i64 q = q0 + u * stride;
-            r[u] = q / qpr;
-            c[u] = (q - r[u] * qpr) << 2;
-            if (q < total && c[u] + 4 <= cols) {
-                const float* sp = src + r[u] * ld_src + c[u];
-                if (SRC_VEC) {
-                    v[u] = __ldcs(reinterpret_cast<const float4*>(sp));
-                } else {
-                    v[u] = make_float4(__ldcs(sp), __ldcs(sp + 1), __ldcs(sp + 2), __ldcs(sp + 3));
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const i64 q = q0 + u * stride;
-            if (q >= total) break;
-            D* dp = dst + r[u] * ld_dst + c[u];
-            if (c[u] + 4 <= cols) {
-                store4(dp, v[u].x, v[u].y, v[u].z, v[u].w, true);
-            } else {
-                const float* sp = src + r[u] * ld_src;
-                for (i64 j = c[u]; j < cols; ++j) store1(dst + r[u] * ld_dst + j, sp[j]);
+            if (q < a.quads) {
+                convert_quad(a, q);
+            } else if (q < total) {
+                convert_quad(b, q - a.quads);
             }
         }
     }
@@ -667,16 +677,12 @@ inline size_t workspace_bytes(i64 M, i64 N, i64 K, int ta, int tb) {
 }
 
 template <int KIND>
-inline int launch_convert(typename Elem<KIND>::T* dst, i64 ld_dst, const float* src, i64 ld_src, i64 rows, i64 cols,
-                          cudaStream_t stream) {
-    typedef typename Elem<KIND>::T D;
-    const bool src_vec = (ld_src % 4 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0);
-    const i64 total = rows * ((cols + 3) / 4);
+inline int launch_converts(const ConvertJob<typename Elem<KIND>::T>& a, const ConvertJob<typename Elem<KIND>::T>& b,
+                           cudaStream_t stream) {
+    const i64 total = a.quads + b.quads;
+    if (total == 0) return AG_OK;
     const unsigned blocks = (unsigned)std::max<i64>(1, std::min<i64>((total + 1023) / 1024, (i64)sm_count() * 8));
-    if (src_vec)
-        tc_convert_kernel<D, true><<<blocks, 256, 0, stream>>>(dst, ld_dst, src, ld_src, (int)rows, (int)cols);
-    else
-        tc_convert_kernel<D, false><<<blocks, 256, 0, stream>>>(dst, ld_dst, src, ld_src, (int)rows, (int)cols);
+    tc_convert_kernel<typename Elem<KIND>::T><<<blocks, 256, 0, stream>>>(a, b);
     return cudaGetLastError() == cudaSuccess ? AG_OK : AG_ERR_CUDA;
 }
 
@@ -687,19 +693,29 @@ inline int tc_fail(const GemmCall& c, int code, const char* msg) {
 
 // Stage one operand for the TMA: bf16 always converts into the workspace;
 // tf32 reads the caller's fp32 matrix in place when its base and row stride
-// are 16-byte aligned, else copies it to a re-strided buffer.
+// are 16-byte aligned, else copies it to a re-strided buffer.  Returns the
+// conversion job (quads = 0 when the operand is read in place).
 template <int KIND>
-inline int stage_operand(const float* src, i64 ld_src, OperandLayout lay, void* ws, const void** base, i64* ld,
-                         cudaStream_t stream) {
+inline ConvertJob<typename Elem<KIND>::T> plan_operand(const float* src, i64 ld_src, OperandLayout lay, void* ws,
+                                                       const void** base, i64* ld) {
     typedef typename Elem<KIND>::T T;
+    ConvertJob<T> j{};
     if (KIND == KIND_TF32 && ld_src % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
         *base = src;
         *ld = ld_src;
-        return AG_OK;
+        return j;
     }
     *ld = staged_ld<KIND>(lay.cols);
     *base = ws;
-    return launch_convert<KIND>(static_cast<T*>(ws), *ld, src, ld_src, lay.rows, lay.cols, stream);
+    j.dst = static_cast<T*>(ws);
+    j.ld_dst = *ld;
+    j.src = src;
+    j.ld_src = ld_src;
+    j.rows = lay.rows;
+    j.cols = lay.cols;
+    j.quads = lay.rows * ((lay.cols + 3) / 4);
+    j.vec = (ld_src % 4 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+    return j;
 }
 
 // CTAS = 1: config bm = 128; CTAS = 2: bm = 256 on a CTA pair
@@ -721,11 +737,11 @@ int launch_tc(const GemmCall& c) {
     char* wsB = wsA ? wsA + round_up_i(la.rows * staged_ld<KIND>(la.cols) * (i64)sizeof(T), 1024) : nullptr;
     const void *baseA = nullptr, *baseB = nullptr;
     i64 ldA = 0, ldB = 0;
-    int r = stage_operand<KIND>(static_cast<const float*>(c.A), c.lda, la, wsA, &baseA, &ldA, c.stream);
-    if (r == AG_OK) r = stage_operand<KIND>(static_cast<const float*>(c.B), c.ldb, lb, wsB, &baseB, &ldB, c.stream);
-    if (r) return tc_fail(c, r, "staging of an operand failed");
-    if ((baseA == (const void*)wsA || baseB == (const void*)wsB) && (c.ws_bytes < need || c.ws == nullptr))
+    const auto jobA = plan_operand<KIND>(static_cast<const float*>(c.A), c.lda, la, wsA, &baseA, &ldA);
+    const auto jobB = plan_operand<KIND>(static_cast<const float*>(c.B), c.ldb, lb, wsB, &baseB, &ldB);
+    if ((jobA.quads || jobB.quads) && (c.ws_bytes < need || c.ws == nullptr))
         return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
+    if (launch_converts<KIND>(jobA, jobB, c.stream) != AG_OK) return tc_fail(c, AG_ERR_CUDA, "staging of the operands failed");
 
     // A: K-major unless transA; B: MN-major unless transB.  Boxes are per
     // CTA: 128 rows of A, BN / CTAS rows of B.
