@@ -328,6 +328,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer (every CTA stages its own share)
+            // programmatic dependent launch: the setup above (barriers, TMEM,
+            // tensormap prefetch) overlapped the staging convert's tail; no
+            // operand byte is read before the upstream grid has completed.
+            // Every other read / write of this kernel (C, out) happens after
+            // the first full barrier, i.e. after this wait.
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
             int stage = 0;
             uint32_t phase = 0;
             for (int t = unit; t < tiles; t += units) {
@@ -585,6 +591,8 @@ __device__ __forceinline__ void convert_quad(const ConvertJob<D>& j, i64 q) {
 template <typename D>
 __global__ void __launch_bounds__(256)
 tc_convert_kernel(const ConvertJob<D> a, const ConvertJob<D> b) {
+    // let the tc_gemm launch (programmatic dependent launch) start its setup
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const i64 total = a.quads + b.quads;
     const i64 stride = (i64)gridDim.x * blockDim.x;
     for (i64 q0 = (i64)blockIdx.x * blockDim.x + threadIdx.x; q0 < total; q0 += 4 * stride) {
@@ -789,13 +797,15 @@ int launch_tc(const GemmCall& c) {
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CTAS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, kernel, mapA, mapB, p) != cudaSuccess)
         return tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
     return cudaGetLastError() == cudaSuccess ? AG_OK : tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
