@@ -802,10 +802,12 @@ int launch_tc(const GemmCall& c) {
     attr[0].val.clusterDim.x = CTAS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // dependent launch only behind this call's own staging convert: the
+    // family path's first kernel never overlaps whatever the caller queued
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = (jobA.quads || jobB.quads) ? 2 : 1;
     if (cudaLaunchKernelEx(&cfg, kernel, mapA, mapB, p) != cudaSuccess)
         return tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
     return cudaGetLastError() == cudaSuccess ? AG_OK : tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
