@@ -590,6 +590,8 @@ def run_ours(args):
                }
 
     launches = sum(pack_launches(c.shape, cfg) for c, cfg in zip(cases, dt_cfgs)) * args.steps
+    # the compiled decision tree's host cost per dispatch (ag_select_bench_ns)
+    select_ns = statistics.median(selector.bench_ns(*c.shape.mnk, reps=20000) for c in cases)
     value = value_1 * world  # replicas: whole-job aggregate over N GPUs
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
@@ -638,6 +640,7 @@ def run_ours(args):
         "sweep": sweep_doc,
         "clocks": clocks,
         "gpu_launches": launches,
+        "dispatch_select_ns": round(select_ns, 1),
         "parity_spot_check_rf": rf,
     }
     if rank == 0:
