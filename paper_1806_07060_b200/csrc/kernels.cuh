@@ -61,6 +61,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// programmatic dependent launch (launch.cuh launch_maybe_dependent): a helper
+// pass lets the next kernel of its family path launch early; that kernel
+// waits here before touching global memory.  Both are no-ops otherwise.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ float fmadd(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fmadd(double a, double b, double c) { return __fma_rn(a, b, c); }
 
@@ -340,6 +346,8 @@ __host__ __device__ constexpr int a_pad() { return AROW ? 4 : 0; }
 template <typename T, int BM_, int BN_, int BK_, int TM, int TN, int UK, int STAGES, bool AROW = false>
 __global__ void __launch_bounds__(cta_threads_bound<T, BM_, BN_, TM, TN>())
 tiled_gemm_kernel(const TiledParams<T> p) {
+    pdl_wait();     // behind this call's packs (dependent launch), else a no-op
+    pdl_trigger();  // the split-K reduction may launch while the last wave runs
     constexpr bool FIXED = BM_ > 0 && BN_ > 0 && BK_ > 0;
     static_assert(!AROW || FIXED, "row-major A needs fixed tiles");
     constexpr int VL = FIXED ? VecW<T>::W : 1;  // elements per cp.async
@@ -554,6 +562,7 @@ tiled_gemm_kernel(const TiledParams<T> p) {
 template <int BM, int BN, int BK, int TM, int TN, int STAGES>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), ((BM / TM) * (BN / TN) >= 256 && TM * TN <= 64) ? 2 : 1)
 inplace_gemm_kernel(const TiledParams<float> p, int K) {
+    pdl_trigger();  // slab path: the reduction kernel may launch early
     static_assert(BK % 4 == 0 && BN % 4 == 0, "16-byte chunks");
     constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY;
     constexpr int LA = BK + 4;  // A stage row stride (floats): 16-byte aligned, odd in chunks when BK % 8 == 0
@@ -772,6 +781,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(const T* __restrict__ partial, int splits, i64 slab, int Np, int M, int N, T alpha, T beta,
                      int use_c, const T* __restrict__ C, i64 ldc, T* __restrict__ out, i64 ldo) {
+    pdl_wait();
     const i64 total = (i64)M * N;
     for (i64 idx = (i64)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
         const int m = (int)(idx / N), n = (int)(idx - (i64)m * N);
@@ -793,6 +803,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 pack_pad_kernel(T* __restrict__ dst, i64 ld_dst, int dst_rows, int dst_cols,
                 const T* __restrict__ src, i64 ld_src, int rows, int cols, int transpose) {
+    pdl_trigger();
     __shared__ T tile[32][33];
     const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
     const int x = threadIdx.x, y = threadIdx.y;
@@ -828,6 +839,7 @@ template <typename T, bool SRC_VEC>
 __global__ void __launch_bounds__(256)
 pack_copy_kernel(T* __restrict__ dst, i64 ld_dst, int dst_rows, int dst_cols, const T* __restrict__ src,
                  i64 ld_src, int rows, int cols) {
+    pdl_trigger();
     constexpr int W = VecW<T>::W;  // elements per 16 bytes
     const i64 qpr = dst_cols / W;
     const i64 total = (i64)dst_rows * qpr;

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <string>
 #include <type_traits>
+#include <utility>
 
 #include "kernels.cuh"
 #include "registry.h"
@@ -34,6 +35,29 @@ inline cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& gran
 }
 
 inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+// Launch `kernel` on `stream`, as a programmatic dependent launch when
+// `dependent` (the previous kernel on the stream is this call's own helper
+// pass, which triggers griddepcontrol.launch_dependents): the launch and CTA
+// setup overlap that helper's tail, and the kernel's griddepcontrol.wait
+// holds every global access until the helper has completed.  The first
+// kernel of a family path is never dependent, so nothing overlaps work the
+// caller queued before the call.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_maybe_dependent(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                          cudaStream_t stream, bool dependent, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = dependent ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 inline int fail(const GemmCall& c, int code, const std::string& msg) {
     if (c.err) *c.err = msg;
@@ -207,10 +231,12 @@ int launch_inplace(const GemmCall& c) {
     if (used_splits > 1) {
         const i64 total = M * N;
         const unsigned blocks = (unsigned)std::min<i64>((total + 255) / 256, 148 * 16);
-        splitk_reduce_kernel<float><<<blocks, 256, 0, c.stream>>>(p.partial, used_splits, Mp * Np, (int)Np, (int)M,
-                                                                   (int)N, p.alpha, p.beta, p.use_c, p.C, c.ldc,
-                                                                   p.out, c.ldo);
-        if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "split-K reduce launch failed");
+        const cudaError_t le = launch_maybe_dependent(
+            splitk_reduce_kernel<float>, dim3(blocks), dim3(256), 0, c.stream, true, (const float*)p.partial,
+            used_splits, (i64)(Mp * Np), (int)Np, (int)M, (int)N, p.alpha, p.beta, p.use_c, p.C, (i64)c.ldc, p.out,
+            (i64)c.ldo);
+        if (le != cudaSuccess || cudaGetLastError() != cudaSuccess)
+            return fail(c, AG_ERR_CUDA, "split-K reduce launch failed");
     }
     return AG_OK;
 }
@@ -278,6 +304,7 @@ int launch_indirect(const GemmCall& c) {
     // op(A)^T, K-major (Kp x Mp): A itself when transA and already padded
     const T* At;
     i64 lda_t;
+    bool packed = false;  // a helper pass precedes the core on the stream
     T* wsA = static_cast<T*>(c.ws);
     T* wsB = reinterpret_cast<T*>(static_cast<char*>(c.ws) + round_up(Kp * Mp * (i64)sizeof(T), 256));
     if (arow) {  // row-major A read in place by the AROW core
@@ -291,6 +318,7 @@ int launch_indirect(const GemmCall& c) {
         if (r) return fail(c, r, "pack of op(A) failed");
         At = wsA;
         lda_t = Mp;
+        packed = true;
     }
     const T* Bp;
     i64 ldb_p;
@@ -302,6 +330,7 @@ int launch_indirect(const GemmCall& c) {
         if (r) return fail(c, r, "pack of op(B) failed");
         Bp = wsB;
         ldb_p = Np;
+        packed = true;
     }
 
     TiledParams<T> p;
@@ -321,21 +350,31 @@ int launch_indirect(const GemmCall& c) {
                                      round_up(Kp * Np * (i64)sizeof(T), 256));
     const dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)used_splits);
     bool launched = false;
+    cudaError_t le = cudaSuccess;
+    // The core is NOT a dependent launch behind its packs: launched early,
+    // its CTAs became resident wherever the pack left room and a single-wave
+    // grid ended up unevenly spread (1024^3 at 64 x 64 tiles: 39 -> 23
+    // TFLOP/s, profiles/r01_pdl_probe.jsonl).  The small split-K reduction
+    // behind it is.
+    (void)packed;
     if constexpr (AROW_OK && FIXED) {
         if (arow) {
-            tiled_gemm_kernel<T, BM, BN, BK, TM, TN, UK, STAGES_AROW, true><<<grid, threads, smem, c.stream>>>(p);
+            le = launch_maybe_dependent(tiled_gemm_kernel<T, BM, BN, BK, TM, TN, UK, STAGES_AROW, true>, grid,
+                                        dim3(threads), smem, c.stream, false, p);
             launched = true;
         }
     }
-    if (!launched) kernel<<<grid, threads, smem, c.stream>>>(p);
-    if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "indirect kernel launch failed");
+    if (!launched) le = launch_maybe_dependent(kernel, grid, dim3(threads), smem, c.stream, false, p);
+    if (le != cudaSuccess || cudaGetLastError() != cudaSuccess)
+        return fail(c, AG_ERR_CUDA, "indirect kernel launch failed");
     if (used_splits > 1) {
         const i64 total = M * N;
         const unsigned blocks = (unsigned)std::min<i64>((total + 255) / 256, 148 * 16);
-        splitk_reduce_kernel<T><<<blocks, 256, 0, c.stream>>>(p.partial, used_splits, Mp * Np, (int)Np, (int)M,
-                                                               (int)N, p.alpha, p.beta, p.use_c, p.C, c.ldc, p.out,
-                                                               c.ldo);
-        if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "split-K reduce launch failed");
+        le = launch_maybe_dependent(splitk_reduce_kernel<T>, dim3(blocks), dim3(256), 0, c.stream, true,
+                                    (const T*)p.partial, used_splits, (i64)(Mp * Np), (int)Np, (int)M, (int)N,
+                                    p.alpha, p.beta, p.use_c, p.C, (i64)c.ldc, p.out, (i64)c.ldo);
+        if (le != cudaSuccess || cudaGetLastError() != cudaSuccess)
+            return fail(c, AG_ERR_CUDA, "split-K reduce launch failed");
     }
     return AG_OK;
 }
