@@ -39,6 +39,8 @@ constexpr size_t smem_bytes() {
 }
 template <int BM, int BN>
 constexpr int stages() {
+    // 3-deep ring (2 CTAs of 128 x 128 per SM); 4 stages measured slower
+    // (fewer resident CTAs), profiles/r01_exp_tiles_tma.jsonl
     return 3 * stage_bytes<BM, BN>() <= 110 * 1024 ? 3 : (2 * stage_bytes<BM, BN>() <= 200 * 1024 ? 2 : 1);
 }
 
