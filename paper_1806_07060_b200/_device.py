@@ -25,11 +25,18 @@ class DeviceUnavailableError(RuntimeError):
     """No CUDA device: the GEMM path has no CPU fallback."""
 
 
+_cuda_ok = False
+
+
 def require_cuda():
+    """torch, after checking (once, then cached) that a CUDA device is visible."""
+    global _cuda_ok
     t = torch()
-    if not t.cuda.is_available():
-        raise DeviceUnavailableError(
-            "no CUDA device visible: adaptgemm-b200 runs GEMMs only on the GPU (sm_100a)")
+    if not _cuda_ok:
+        if not t.cuda.is_available():
+            raise DeviceUnavailableError(
+                "no CUDA device visible: adaptgemm-b200 runs GEMMs only on the GPU (sm_100a)")
+        _cuda_ok = True
     return t
 
 
@@ -89,7 +96,13 @@ def workspace(nbytes: int, device):
 
 
 def current_stream_handle(device) -> int:
+    """Raw cudaStream_t of torch's current stream on `device` (the C++ getter
+    when torch exposes it: no Stream object per call)."""
     t = torch()
+    raw = getattr(t._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        idx = device.index if getattr(device, "index", None) is not None else t.cuda.current_device()
+        return int(raw(idx))
     return int(t.cuda.current_stream(device).cuda_stream)
 
 
