@@ -189,3 +189,25 @@ def test_host_path_errors():
         codegen.dispatch_native(sel, s, A, B, C, out=np.zeros((20, 30), np.float32))
     with pytest.raises(ShapeError):
         codegen.dispatch_native(sel, s, A[:, :5], B, C)
+
+
+def test_host_path_random_shapes_and_panels():
+    """Seeded random shapes / transposes / beta / panel counts: the pipelined
+    host path returns exactly the device path's bits."""
+    import torch
+    from paper_1806_07060_b200 import rng
+    stream = rng.SplitMix64(0x405)
+    names = ["indirect:64-64-16-8-4-1", "splitk:32-32-16-4-4-4", "tma:64-64-32-8-8-1", "direct:16-16-8-2-2-1",
+             "indirect:128-128-32-8-8-1"]
+    caps = DeviceCaps.b200_tc()
+    for case in range(20):
+        m, n, k = (1 + stream.below(700) for _ in range(3))
+        s = ProblemShape(m, n, k, alpha=1.0, beta=(0.0, 0.5)[stream.below(2)],
+                         transA=bool(stream.below(2)), transB=bool(stream.below(2)))
+        cfg = KernelConfig.from_canonical(names[stream.below(len(names))])
+        A, B, C = rand_operands(s, seed=case)
+        sel = _one_class_selector(cfg)
+        dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+        ref, _, _ = codegen.dispatch_native(sel, s, dA, dB, dC, caps)
+        got, _, _ = codegen.dispatch_native(sel, s, A, B, C, caps, panels=1 + stream.below(5))
+        np.testing.assert_array_equal(got, ref.cpu().numpy(), err_msg=f"{s} {cfg.canonical()}")
