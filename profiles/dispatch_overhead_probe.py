@@ -19,5 +19,5 @@ torch.cuda.synchronize(); t0 = time.perf_counter()
 for _ in range(200): codegen.dispatch_native(sel, s, dA, dB, dC, caps, out=dO)
 torch.cuda.synchronize(); print("device-path call us", (time.perf_counter() - t0) / 200 * 1e6)
 pr = cProfile.Profile(); pr.enable()
-for _ in range(200): codegen.dispatch_native(sel, s, A, B, C, caps, out=out)
-pr.disable(); pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+for _ in range(200): codegen.dispatch_native(sel, s, dA, dB, dC, caps, out=dO)
+pr.disable(); pstats.Stats(pr).sort_stats("tottime").print_stats(22)
