@@ -71,9 +71,36 @@ def geomean(xs):
 # model: the reference pipeline on the shipped B200 tables
 
 
-def build_model():
+def _pipeline(tables, provenance):
+    """The reference pipeline on a list of tables (cli.py:281-373): dataset,
+    seeded 80/20 split, the 5 x 8 CART grid on the train split, the model
+    with the best test DTPR."""
     from paper_1806_07060_b200 import evaluation, model
     from paper_1806_07060_b200.dataset import dataset_from_tables, split
+
+    ds = dataset_from_tables(tables, provenance)
+    sp = split(ds, SPLIT_FRACTION, SPLIT_SEED)
+    recs = ds.features_and_labels()
+    train_recs = [recs[i] for i in sp.train]
+    test_recs = [recs[i] for i in sp.test]
+    named = model.grid_train(train_recs)
+    by_shape = evaluation.tables_by_shape(tables)
+    policy = evaluation.build_baseline_policy(by_shape[(256, 256, 256)], by_shape[(1024, 1024, 1024)],
+                                              384).register(ds.class_index)
+    scores = evaluation.score_models(named, test_recs, by_shape, ds.class_index, policy)
+    best = evaluation.select_best_model(scores)
+    return {"tree": dict(named)[best.name], "name": best.name, "classes": ds.class_index, "policy": policy,
+            "train": {mnk for mnk, _ in train_recs}, "test": {mnk for mnk, _ in test_recs},
+            "score": {"accuracy": best.accuracy, "dtpr": best.dtpr, "dttr": best.dttr,
+                      "leaves": best.stats.total_leaves, "height": best.stats.height},
+            "n_train": len(train_recs), "n_test": len(test_recs)}
+
+
+def build_model():
+    """The headline model: the reference pipeline on the po2 tables ONLY
+    (SURVEY.md 8(d) C3: train on po2, evaluate on the DeepBench-style set);
+    no DeepBench table is seen in training or model selection.  The
+    DeepBench tables provide the oracle per shape."""
     from paper_1806_07060_b200.kernels import KernelFamily
     from paper_1806_07060_b200.tuner import load_table_bundle
 
@@ -83,37 +110,37 @@ def build_model():
     db = load_table_bundle(DB_BUNDLE)
     by_shape = {t.shape.mnk: t for t in po2}
     by_shape.update({t.shape.mnk: t for t in db})
-    # the reference CLI's "hybrid" dataset (cli.py:166-179): po2 + DeepBench
-    # shapes deduplicated in order, one seeded 80/20 split; the tree is
-    # scored and selected on the held-out 20 % (cmd_train / cmd_eval)
+    pipe = _pipeline(po2, "po2")
+    return {
+        "tree": pipe["tree"], "name": pipe["name"], "classes": pipe["classes"], "policy": pipe["policy"],
+        "tables": by_shape, "po2_test": [t.shape for t in po2 if t.shape.mnk in pipe["test"]],
+        "db_all": [t.shape for t in db],
+        # DeepBench shapes that are not po2 training shapes (a po2 grid point such
+        # as 2048 x 16 x 2048 can coincide with a DeepBench shape)
+        "db_unseen": [t.shape for t in db if t.shape.mnk not in pipe["train"]],
+        "score": pipe["score"], "n_train": pipe["n_train"], "n_test": pipe["n_test"],
+        "train_set": "po2 train split (seed 2024, 80 %)", "family_direct": KernelFamily.DIRECT,
+    }
+
+
+def build_hybrid_model():
+    """Secondary model: the reference CLI's "hybrid" dataset (cli.py:166-179),
+    po2 + DeepBench deduplicated in order, one seeded 80/20 split; reported
+    with its train and test subsets separately (cli.py:413-420)."""
+    from paper_1806_07060_b200.tuner import load_table_bundle
+
+    po2 = load_table_bundle(PO2_BUNDLE)
+    db = load_table_bundle(DB_BUNDLE)
     hybrid, seen = [], set()
     for t in po2 + db:
         if t.shape.mnk not in seen:
             seen.add(t.shape.mnk)
             hybrid.append(t)
-    ds = dataset_from_tables(hybrid, "hybrid")
-    sp = split(ds, SPLIT_FRACTION, SPLIT_SEED)
-    recs = ds.features_and_labels()
-    train_recs = [recs[i] for i in sp.train]
-    test_recs = [recs[i] for i in sp.test]
-    test_set = {recs[i][0] for i in sp.test}
-    n_train = len(train_recs)
-    named = model.grid_train(train_recs)
-    anchor_d, anchor_i = by_shape[(256, 256, 256)], by_shape[(1024, 1024, 1024)]
-    policy = evaluation.build_baseline_policy(anchor_d, anchor_i, 384).register(ds.class_index)
-    tables = evaluation.tables_by_shape(hybrid)
-    scores = evaluation.score_models(named, test_recs, tables, ds.class_index, policy)
-    best = evaluation.select_best_model(scores)
-    tree = dict(named)[best.name]
-    return {
-        "tree": tree, "name": best.name, "classes": ds.class_index, "policy": policy,
-        "tables": by_shape, "po2_test": [t.shape for t in po2 if t.shape.mnk in test_set],
-        "db_all": [t.shape for t in db], "db_test": [t.shape for t in db if t.shape.mnk in test_set],
-        "score": {"accuracy": best.accuracy, "dtpr": best.dtpr, "dttr": best.dttr,
-                  "leaves": best.stats.total_leaves, "height": best.stats.height},
-        "n_train": n_train, "n_test": len(test_recs),
-        "family_direct": KernelFamily.DIRECT,
-    }
+    pipe = _pipeline(hybrid, "hybrid")
+    db_set = {t.shape.mnk for t in db}
+    pipe["db_train"] = [ProblemShapeOf(mnk) for mnk in sorted(pipe["train"] & db_set)]
+    pipe["db_test"] = [ProblemShapeOf(mnk) for mnk in sorted(pipe["test"] & db_set)]
+    return pipe
 
 
 def build_tc_model(policy):

@@ -134,6 +134,25 @@ int ag_gemm_host(const ag_shape* shape, const ag_config* config, const ag_caps* 
                  const void* C, int64_t ldc, void* out, int64_t ldo,
                  void* device_scratch, size_t scratch_bytes, int panels, void* stream);
 
+/* ag_gemm_host with options.  flags & AG_HOST_REGISTER: page-lock the
+ * caller's host buffers (>= 1 MB) for the duration of the call, so pageable
+ * numpy memory gets pinned-rate copies that overlap the kernels.
+ * device_scratch == NULL: use the library's own grow-only scratch
+ * (ag_device_scratch).  *kernel_seconds (if not NULL) receives the device
+ * time of the family path (CUDA events around each panel's kernels, summed),
+ * the reference's `seconds` without the copies. */
+#define AG_HOST_REGISTER 1
+int ag_gemm_host_ex(const ag_shape* shape, const ag_config* config, const ag_caps* caps, int dtype,
+                    const void* A, int64_t lda, const void* B, int64_t ldb,
+                    const void* C, int64_t ldc, void* out, int64_t ldo,
+                    void* device_scratch, size_t scratch_bytes, int panels, int flags, void* stream,
+                    double* kernel_seconds);
+
+/* per-thread, per-device grow-only device buffer owned by the library
+ * (cudaMalloc; NULL on failure).  Lets a caller without a device allocator
+ * (the reference's numpy-only package) drive the host path. */
+void* ag_device_scratch(size_t bytes);
+
 /* ag_gemm timed on the device: `warmup` untimed runs then `repeats` timed
  * samples (CUDA events on `stream`); each sample is the mean of `inner`
  * back-to-back runs replayed from one CUDA graph (inner <= 0: chosen so a
@@ -155,6 +174,17 @@ int ag_tune(const ag_shape* shape, const ag_config* configs, int n_configs,
             const void* C, int64_t ldc, void* out, int64_t ldo,
             void* workspace, size_t workspace_bytes, void* stream,
             int warmup, int repeats, double* elapsed_s, int* failed_index);
+
+/* ag_tune with a choice of timing regime.  l2_flush = 0: ag_tune's warm,
+ * graph-replayed back-to-back samples; l2_flush = 1: every sample is one
+ * family path after a 256 MB write has evicted L2 (the regime bench.py
+ * reports), so labels and the metric are measured the same way. */
+int ag_tune_ex(const ag_shape* shape, const ag_config* configs, int n_configs,
+               const ag_caps* caps, int dtype,
+               const void* A, int64_t lda, const void* B, int64_t ldb,
+               const void* C, int64_t ldc, void* out, int64_t ldo,
+               void* workspace, size_t workspace_bytes, void* stream,
+               int warmup, int repeats, int l2_flush, double* elapsed_s, int* failed_index);
 
 /* replaces kernels.gemm_reference / _kernel_reference (kernels.py:184-195,
  * 294-301): textbook (i,j,k) GEMM, float64 accumulation in k order with
@@ -240,6 +270,14 @@ int ag_dispatch_gemm_host(const ag_selector* sel, const ag_config* fallback,
                           const void* C, int64_t ldc, void* out, int64_t ldo,
                           void* device_scratch, size_t scratch_bytes, int panels, void* stream,
                           ag_config* selected, int* used_fallback);
+
+/* ag_dispatch_gemm_host with ag_gemm_host_ex's flags and kernel time. */
+int ag_dispatch_gemm_host_ex(const ag_selector* sel, const ag_config* fallback,
+                             const ag_shape* shape, const ag_caps* caps, int dtype,
+                             const void* A, int64_t lda, const void* B, int64_t ldb,
+                             const void* C, int64_t ldc, void* out, int64_t ldo,
+                             void* device_scratch, size_t scratch_bytes, int panels, int flags, void* stream,
+                             ag_config* selected, int* used_fallback, double* kernel_seconds);
 
 #ifdef __cplusplus
 }

@@ -78,13 +78,20 @@ def leading_dim(t) -> int:
 _tls = threading.local()
 
 
-def workspace(nbytes: int, device):
-    """Per-thread, per-device grow-only byte buffer (allocation is never timed)."""
+def workspace(nbytes: int, device, stream: int | None = None):
+    """Per-thread, per-device, per-stream grow-only byte buffer (allocation is
+    never timed).  Keyed by the stream the family path runs on: two calls
+    on different streams never share pack / split-K buffers, and a buffer
+    is allocated while its stream is torch's current one, so the caching
+    allocator only hands a freed (outgrown) buffer back to work on that
+    same stream, ordered after the kernels that used it."""
     t = torch()
     cache = getattr(_tls, "ws", None)
     if cache is None:
         cache = _tls.ws = {}
-    key = (device.type, device.index)
+    if stream is None:
+        stream = current_stream_handle(device)
+    key = (device.type, device.index, int(stream))
     buf = cache.get(key)
     if buf is None or buf.numel() < nbytes:
         size = max(nbytes, 1 << 20)
@@ -93,6 +100,28 @@ def workspace(nbytes: int, device):
         buf = t.empty(size, dtype=t.uint8, device=device)
         cache[key] = buf
     return buf
+
+
+class _NoGuard:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_GUARD = _NoGuard()
+
+
+def guard(device):
+    """Make `device` the current CUDA device for a native call (kernel
+    launches, events and attributes follow the current device); a no-op when
+    it already is."""
+    t = torch()
+    idx = device.index if getattr(device, "index", None) is not None else None
+    if idx is None or idx == t.cuda.current_device():
+        return _NO_GUARD
+    return t.cuda.device(idx)
 
 
 def current_stream_handle(device) -> int:

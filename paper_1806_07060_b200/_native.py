@@ -13,6 +13,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libadaptgemm_b200.so"
 
 AG_OK, AG_ERR_CONFIG, AG_ERR_SHAPE, AG_ERR_CUDA = 0, 1, 2, 3
+AG_HOST_REGISTER = 1  # ag_gemm_host_ex flag: page-lock the caller's host buffers for the call
 AG_FAMILY_DIRECT, AG_FAMILY_INDIRECT, AG_FAMILY_SPLITK = 0, 1, 2
 AG_FAMILY_TF32, AG_FAMILY_BF16 = 3, 4
 AG_FAMILY_TMA = 5
@@ -57,6 +58,9 @@ SIGNATURES = {
     "ag_tune": (c_int, [POINTER(AgShape), POINTER(AgConfig), c_int, POINTER(AgCaps), c_int,
                         _P, c_int64, _P, c_int64, _P, c_int64, _P, c_int64, _P, c_size_t, _P,
                         c_int, c_int, POINTER(c_double), POINTER(c_int)]),
+    "ag_tune_ex": (c_int, [POINTER(AgShape), POINTER(AgConfig), c_int, POINTER(AgCaps), c_int,
+                           _P, c_int64, _P, c_int64, _P, c_int64, _P, c_int64, _P, c_size_t, _P,
+                           c_int, c_int, c_int, POINTER(c_double), POINTER(c_int)]),
     "ag_gemm_reference": (c_int, [POINTER(AgShape), c_int, _P, c_int64, _P, c_int64,
                                   _P, c_int64, _P, c_int64, _P]),
     "ag_pack_padded": (c_int, [c_int, _P, c_int64, c_int64, c_int64, c_int, _P, c_int64, c_int64, _P]),
@@ -82,6 +86,11 @@ SIGNATURES = {
                                  POINTER(AgConfig), POINTER(c_int)]),
     "ag_host_scratch_bytes": (c_size_t, [POINTER(AgShape), POINTER(AgConfig), c_int, c_int]),
     "ag_gemm_host": (c_int, _GEMM_ARGS[:-1] + [c_int, _P]),
+    "ag_gemm_host_ex": (c_int, _GEMM_ARGS[:-1] + [c_int, c_int, _P, POINTER(c_double)]),
+    "ag_device_scratch": (c_void_p, [c_size_t]),
+    "ag_dispatch_gemm_host_ex": (c_int, [c_void_p, POINTER(AgConfig), POINTER(AgShape), POINTER(AgCaps), c_int,
+                                         _P, c_int64, _P, c_int64, _P, c_int64, _P, c_int64, _P, c_size_t, c_int,
+                                         c_int, _P, POINTER(AgConfig), POINTER(c_int), POINTER(c_double)]),
     "ag_dispatch_gemm_host": (c_int, [c_void_p, POINTER(AgConfig), POINTER(AgShape), POINTER(AgCaps), c_int,
                                       _P, c_int64, _P, c_int64, _P, c_int64, _P, c_int64, _P, c_size_t, c_int, _P,
                                       POINTER(AgConfig), POINTER(c_int)]),

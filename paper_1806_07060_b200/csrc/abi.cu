@@ -66,36 +66,60 @@ bool in_range(const ag_config& c) {
            c.bk < 512 && c.tm < 64 && c.tn < 64 && c.uk <= 64;
 }
 
-// exact instantiation, else the run-time-tile kernel for (tm, tn) -- register
-// tiles wider than 8 (the B200 wide tiles in float64, or configs outside the
-// domains) run the 8-wide one: the tile shape only distributes the output
-// elements over threads, every element's K order is the same; the split-K
-// family runs the indirect core (unroll 1) with a K-slice grid axis
+// thread bound of a run-time-tile kernel (kernels.cuh cta_threads_bound<T, 0, 0, TM, TN>)
+int runtime_thread_bound(int dtype, int tm, int tn) {
+    const int regs = tm * tn * (dtype == AG_F64 ? 2 : 1);
+    return regs >= 32 ? 256 : (regs >= 16 ? 512 : 1024);
+}
+
+// The run-time-tile kernel (any bm / bn / bk) for a config: the (tm, tn)
+// one when its thread bound admits the config's CTA, else the smallest
+// larger register tile from {1, 2, 4, 8}^2 (and the 8 x 16 / 16 x 8 wide
+// ones) that divides the CTA tile and fits.  The register tile only
+// distributes the output elements over threads; every element sees the same
+// K order, so the result is the same.  This is how float64 runs every
+// config the float32 space makes legal (float64 register tiles are twice as
+// large, so their kernels allow fewer threads per CTA).
+ag::LaunchFn find_runtime(const ag_config& c, int family, int dtype) {
+    auto& m = registry().map;
+    static const int tiles[][2] = {{1, 1}, {1, 2}, {2, 1}, {2, 2}, {1, 4}, {4, 1}, {2, 4}, {4, 2}, {1, 8}, {8, 1},
+                                   {4, 4}, {2, 8}, {8, 2}, {4, 8}, {8, 4}, {8, 8}, {8, 16}, {16, 8}};
+    // exact (tm, tn) first when it exists and fits
+    auto fits = [&](int tm, int tn) {
+        return c.bm % tm == 0 && c.bn % tn == 0 && (c.bm / tm) * (c.bn / tn) <= runtime_thread_bound(dtype, tm, tn);
+    };
+    if (fits(c.tm, c.tn)) {
+        auto it = m.find(make_key(family, dtype, 0, 0, 0, c.tm, c.tn, 0));
+        if (it != m.end()) return it->second;
+    }
+    for (const auto& t : tiles) {
+        if (t[0] < std::min(c.tm, 8) || t[1] < std::min(c.tn, 8) || !fits(t[0], t[1])) continue;
+        auto it = m.find(make_key(family, dtype, 0, 0, 0, t[0], t[1], 0));
+        if (it != m.end()) return it->second;
+    }
+    return nullptr;
+}
+
+// exact instantiation, else a run-time-tile kernel (find_runtime); the
+// split-K family runs the indirect core (unroll 1) with a K-slice grid axis
 ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
     if (!in_range(c)) return nullptr;
     auto& m = registry().map;
-    const int rtm = std::min(c.tm, 8), rtn = std::min(c.tn, 8);
     if (c.family == AG_FAMILY_SPLITK) {
         auto it = m.find(make_key(AG_FAMILY_SPLITK, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, 0));
         if (it != m.end()) return it->second;
         it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, 1));
         if (it != m.end()) return it->second;
-        it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, 0, 0, 0, rtm, rtn, 0));
-        return it != m.end() ? it->second : nullptr;
+        return find_runtime(c, AG_FAMILY_INDIRECT, dtype);
     }
     if (c.family == AG_FAMILY_TMA) {  // float32: its own launcher; float64: the indirect run-time-tile kernel
         auto it = m.find(make_key(AG_FAMILY_TMA, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk));
         if (it != m.end()) return it->second;
-        it = m.find(make_key(AG_FAMILY_INDIRECT, dtype, 0, 0, 0, rtm, rtn, 0));
-        return it != m.end() ? it->second : nullptr;
+        return find_runtime(c, AG_FAMILY_INDIRECT, dtype);
     }
     auto it = m.find(make_key(c.family, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk));
     if (it != m.end()) return it->second;
-    it = m.find(make_key(c.family, dtype, 0, 0, 0, c.tm, c.tn, 0));
-    if (it != m.end()) return it->second;
-    it = m.find(make_key(c.family, dtype, 0, 0, 0, rtm, rtn, 0));
-    if (it != m.end()) return it->second;
-    return nullptr;
+    return find_runtime(c, c.family, dtype);
 }
 
 std::string config_str(const ag_config& c) {
@@ -171,6 +195,15 @@ __global__ void spin_kernel(long long ns) {
 struct TimingRes {
     cudaStream_t cap = nullptr;
     std::vector<cudaEvent_t> ev;
+    void* flush = nullptr;  // > L2 (126 MB) scratch written before every cold sample
+    static constexpr size_t kFlushBytes = 256ull << 20;
+    void* flush_buffer() {
+        if (!flush && cudaMalloc(&flush, kFlushBytes) != cudaSuccess) {
+            cudaGetLastError();
+            flush = nullptr;
+        }
+        return flush;
+    }
     ~TimingRes() {
         // process teardown: the driver may be gone already; ignore errors
     }
@@ -187,7 +220,12 @@ struct TimingRes {
         return cap;
     }
 };
-thread_local TimingRes t_res;
+// per thread and per device: events and streams belong to the device that
+// was current when they were created
+TimingRes& res() {
+    thread_local TimingRes r[ag::kMaxDevices];
+    return r[ag::current_device()];
+}
 
 double median_of(std::vector<double> v) {
     std::sort(v.begin(), v.end());
@@ -195,15 +233,22 @@ double median_of(std::vector<double> v) {
     return (n % 2) ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
 }
 
-int timed_run(const ag::GemmCall& call, ag::LaunchFn fn, int warmup, int repeats, int inner, double* median_s) {
+// Median device time of one family path.  Warm mode (l2_flush = 0): each
+// sample is `inner` back-to-back paths replayed from one CUDA graph (inner
+// auto-sized to ~50 us), operands L2-resident.  Cold mode (l2_flush = 1):
+// each sample is ONE path after a 256 MB write has evicted L2, the regime
+// bench.py measures; the flush runs before the start event.
+int timed_run(const ag::GemmCall& call, ag::LaunchFn fn, int warmup, int repeats, int inner, double* median_s,
+              int l2_flush = 0) {
     if (repeats < 1) return set_err(AG_ERR_SHAPE, "repeats must be >= 1");
     cudaStream_t st = call.stream;
+    if (l2_flush) inner = 1;
     // warmup runs (>= 1: also sets kernel attributes before graph capture)
     for (int w = 0; w < std::max(warmup, 1); ++w) {
         int r = fn(call);
         if (r) return r;
     }
-    cudaEvent_t e0 = t_res.event(0), e1 = t_res.event(1);
+    cudaEvent_t e0 = res().event(0), e1 = res().event(1);
     if (!e0 || !e1) return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
     if (inner <= 0) {
         spin_kernel<<<1, 1, 0, st>>>(20000);
@@ -219,7 +264,7 @@ int timed_run(const ag::GemmCall& call, ag::LaunchFn fn, int warmup, int repeats
         inner = std::min(std::max(inner, 1), 64);
     }
     // capture `inner` back-to-back paths into one graph
-    cudaStream_t cap = t_res.capture_stream();
+    cudaStream_t cap = res().capture_stream();
     if (!cap) return set_err(AG_ERR_CUDA, "cannot create capture stream");
     ag::GemmCall cc = call;
     cc.stream = cap;
@@ -238,14 +283,20 @@ int timed_run(const ag::GemmCall& call, ag::LaunchFn fn, int warmup, int repeats
     ce = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (ce != cudaSuccess) return set_err(AG_ERR_CUDA, std::string("graph instantiate failed: ") + cudaGetErrorString(ce));
+    void* fbuf = nullptr;
+    if (l2_flush && !(fbuf = res().flush_buffer())) {
+        cudaGraphExecDestroy(exec);
+        return set_err(AG_ERR_CUDA, "cannot allocate the L2 flush buffer");
+    }
     // back the queue up so no sample includes host enqueue gaps
     spin_kernel<<<1, 1, 0, st>>>(20000 + 4000LL * repeats);
     for (int r = 0; r < repeats; ++r) {
-        cudaEvent_t a = t_res.event(2 + 2 * r), b = t_res.event(3 + 2 * r);
+        cudaEvent_t a = res().event(2 + 2 * r), b = res().event(3 + 2 * r);
         if (!a || !b) {
             cudaGraphExecDestroy(exec);
             return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
         }
+        if (fbuf) cudaMemsetAsync(fbuf, r & 0xff, TimingRes::kFlushBytes, st);
         cudaEventRecord(a, st);
         cudaGraphLaunch(exec, st);
         cudaEventRecord(b, st);
@@ -256,7 +307,7 @@ int timed_run(const ag::GemmCall& call, ag::LaunchFn fn, int warmup, int repeats
     std::vector<double> samples(repeats);
     for (int r = 0; r < repeats; ++r) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, t_res.ev[2 + 2 * r], t_res.ev[3 + 2 * r]);
+        cudaEventElapsedTime(&ms, res().ev[2 + 2 * r], res().ev[3 + 2 * r]);
         samples[r] = (double)ms * 1e-3 / inner;
     }
     *median_s = std::max(median_of(samples), 1e-9);
@@ -292,6 +343,17 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, f
 struct HostPipe {
     cudaStream_t s[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> ev;
+    std::vector<cudaEvent_t> tev;  // timing events around each panel's family path
+    void* scratch = nullptr;       // ag_device_scratch: grow-only, per thread and device
+    size_t scratch_bytes = 0;
+    cudaEvent_t timing_event(size_t i) {
+        while (tev.size() <= i) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+            tev.push_back(e);
+        }
+        return tev[i];
+    }
     bool ok() {
         for (auto& x : s)
             if (!x && cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return false;
@@ -306,7 +368,10 @@ struct HostPipe {
         return ev[i];
     }
 };
-thread_local HostPipe t_pipe;
+HostPipe& pipe() {
+    thread_local HostPipe p[ag::kMaxDevices];
+    return p[ag::current_device()];
+}
 
 constexpr int64_t kHostAlign = 256;
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -362,7 +427,33 @@ inline cudaError_t copy2d(void* dst, int64_t dpitch, const void* src, int64_t sp
     return cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)rows, kind, st);
 }
 
+// Page-lock caller host buffers for one call so their copies run as DMA at
+// the pinned rate and overlap the kernels; buffers that are already pinned
+// (or cannot be registered) are left alone and copied as they are.
+struct HostLocks {
+    std::vector<void*> held;
+    void lock(const void* p, int64_t rows, int64_t ld, int64_t cols, int64_t elem) {
+        if (!p || rows <= 0 || cols <= 0) return;
+        const size_t bytes = (size_t)(((rows - 1) * ld + cols) * elem);
+        if (bytes < (1u << 20)) return;  // small: registration costs more than it saves
+        void* q = const_cast<void*>(p);
+        if (cudaHostRegister(q, bytes, cudaHostRegisterDefault) == cudaSuccess)
+            held.push_back(q);
+        else
+            cudaGetLastError();
+    }
+    ~HostLocks() {
+        for (void* q : held) cudaHostUnregister(q);
+        cudaGetLastError();
+    }
+};
+
 }  // namespace
+
+namespace ag {
+int set_last_error(int code, const std::string& msg) { return set_err(code, msg); }
+std::string config_string(const ag_config& c) { return config_str(c); }
+}  // namespace ag
 
 extern "C" {
 
@@ -438,16 +529,56 @@ size_t ag_host_scratch_bytes(const ag_shape* s, const ag_config* c, int dtype, i
     return h.total;
 }
 
+void* ag_device_scratch(size_t bytes) {
+    HostPipe& hp = pipe();
+    if (bytes <= hp.scratch_bytes && hp.scratch) return hp.scratch;
+    if (hp.scratch) {
+        cudaDeviceSynchronize();  // the old block may still be in use by queued copies
+        cudaFree(hp.scratch);
+        hp.scratch = nullptr;
+        hp.scratch_bytes = 0;
+    }
+    const size_t want = std::max<size_t>(bytes, 1u << 20);
+    if (cudaMalloc(&hp.scratch, want) != cudaSuccess) {
+        cudaGetLastError();
+        hp.scratch = nullptr;
+        set_err(AG_ERR_CUDA, "cudaMalloc of the host-path scratch failed");
+        return nullptr;
+    }
+    hp.scratch_bytes = want;
+    return hp.scratch;
+}
+
 int ag_gemm_host(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A, int64_t lda,
                  const void* B, int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo, void* dev,
                  size_t dev_bytes, int panels, void* stream) {
+    return ag_gemm_host_ex(s, c, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, dev, dev_bytes, panels, 0, stream,
+                           nullptr);
+}
+
+int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A,
+                    int64_t lda, const void* B, int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo,
+                    void* dev, size_t dev_bytes, int panels, int flags, void* stream, double* kernel_seconds) {
     ag::LaunchFn fn = nullptr;
     int r = prepare(s, c, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, &fn);
     if (r) return r;
     HostPlan h;
     plan_host(s, c, dtype, panels, &h);
-    if (!dev || dev_bytes < h.total) return set_err(AG_ERR_SHAPE, "device scratch too small for the host path");
+    if (!dev) {  // the library's own scratch
+        dev = ag_device_scratch(h.total);
+        dev_bytes = dev ? std::max<size_t>(h.total, 1) : 0;
+        if (!dev) return AG_ERR_CUDA;
+    }
+    if (dev_bytes < h.total) return set_err(AG_ERR_SHAPE, "device scratch too small for the host path");
+    HostPipe& t_pipe = pipe();
     if (!t_pipe.ok()) return set_err(AG_ERR_CUDA, "cannot create the host-path streams");
+    HostLocks locks;
+    if (flags & AG_HOST_REGISTER) {
+        locks.lock(A, h.ra, lda, h.ca, h.elem);
+        locks.lock(B, h.rb, ldb, h.cb, h.elem);
+        if (h.reads_c) locks.lock(C, s->m, ldc, s->n, h.elem);
+        locks.lock(out, s->m, ldo, s->n, h.elem);
+    }
     cudaStream_t in = t_pipe.s[0], run = t_pipe.s[1], back = t_pipe.s[2];
     char* base = static_cast<char*>(dev);
     char *dA = base + h.offA, *dB = base + h.offB, *dC = base + h.offC, *dO = base + h.offO;
@@ -513,7 +644,11 @@ int ag_gemm_host(const ag_shape* s, const ag_config* c, const ag_caps* caps, int
         }
         ok(cudaEventRecord(ein, in));
         ok(cudaStreamWaitEvent(run, ein, 0));
+        cudaEvent_t k0 = kernel_seconds ? t_pipe.timing_event(2 * p) : nullptr;
+        cudaEvent_t k1 = kernel_seconds ? t_pipe.timing_event(2 * p + 1) : nullptr;
+        if (k0) ok(cudaEventRecord(k0, run));
         r = fn(make_call(&ps, c, dtype, pa, pla, pb, plb, pc, N, po, N, dW, h.wsz, run));
+        if (k1) ok(cudaEventRecord(k1, run));
         if (r) {
             cudaStreamSynchronize(in);
             cudaStreamSynchronize(run);
@@ -532,6 +667,14 @@ int ag_gemm_host(const ag_shape* s, const ag_config* c, const ag_caps* caps, int
     ok(cudaStreamSynchronize(run));
     ok(cudaStreamSynchronize(in));
     if (ce != cudaSuccess) return set_err(AG_ERR_CUDA, std::string("host path: ") + cudaGetErrorString(ce));
+    if (kernel_seconds) {  // device time of the family path, summed over the panels
+        double sum = 0.0;
+        for (int p = 0; p < h.panels; ++p) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, t_pipe.tev[2 * p], t_pipe.tev[2 * p + 1]) == cudaSuccess) sum += ms;
+        }
+        *kernel_seconds = std::max(sum * 1e-3, 1e-9);
+    }
     cudaError_t le = cudaGetLastError();
     return le == cudaSuccess ? AG_OK : set_err(AG_ERR_CUDA, cudaGetErrorString(le));
 }
@@ -550,10 +693,21 @@ int ag_gemm_timed(const ag_shape* s, const ag_config* c, const ag_caps* caps, in
 int ag_tune(const ag_shape* s, const ag_config* configs, int n_configs, const ag_caps* caps, int dtype, const void* A,
             int64_t lda, const void* B, int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo, void* ws,
             size_t ws_bytes, void* stream, int warmup, int repeats, double* elapsed_s, int* failed_index) {
+    return ag_tune_ex(s, configs, n_configs, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, ws, ws_bytes, stream,
+                      warmup, repeats, 0, elapsed_s, failed_index);
+}
+
+int ag_tune_ex(const ag_shape* s, const ag_config* configs, int n_configs, const ag_caps* caps, int dtype,
+               const void* A, int64_t lda, const void* B, int64_t ldb, const void* C, int64_t ldc, void* out,
+               int64_t ldo, void* ws, size_t ws_bytes, void* stream, int warmup, int repeats, int l2_flush,
+               double* elapsed_s, int* failed_index) {
     if (failed_index) *failed_index = -1;
     for (int i = 0; i < n_configs; ++i) {
-        int r = ag_gemm_timed(s, &configs[i], caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, ws, ws_bytes, stream,
-                              warmup, repeats, 0, &elapsed_s[i]);
+        ag::LaunchFn fn = nullptr;
+        int r = prepare(s, &configs[i], caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, &fn);
+        if (!r)
+            r = timed_run(make_call(s, &configs[i], dtype, A, lda, B, ldb, C, ldc, out, ldo, ws, ws_bytes, stream),
+                          fn, warmup, repeats, 0, &elapsed_s[i], l2_flush);
         if (r) {
             if (failed_index) *failed_index = i;
             t_err = "config " + config_str(configs[i]) + ": " + t_err;
@@ -567,9 +721,8 @@ int ag_gemm_reference(const ag_shape* s, int dtype, const void* A, int64_t lda, 
                       const void* C, int64_t ldc, void* out, int64_t ldo, void* stream) {
     int r = check_operands(s, dtype, A, lda, B, ldb, C, ldc, out, ldo);
     if (r) return r;
-    if (s->m > 65535) return set_err(AG_ERR_SHAPE, "gemm_reference supports M <= 65535");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    dim3 grid((unsigned)((s->n + 255) / 256), (unsigned)s->m);
+    dim3 grid((unsigned)((s->n + 255) / 256), (unsigned)std::min<int64_t>(s->m, 65535));
     if (dtype == AG_F32)
         ag::reference_gemm_kernel<float><<<grid, 256, 0, st>>>(
             (int)s->m, (int)s->n, (int)s->k, s->alpha, s->beta, s->trans_a, s->trans_b, (const float*)A, lda,
@@ -603,7 +756,7 @@ int ag_ffma_peak(void* stream, double* tflops) {
     if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return set_err(AG_ERR_CUDA, "cudaMalloc failed");
     const int blocks = sms * 8, threads = 256, iters = 4096;
     ffma_peak_kernel<<<blocks, threads, 0, st>>>(out, 64, 1.000001f, 1e-7f);  // warm
-    cudaEvent_t e0 = t_res.event(0), e1 = t_res.event(1);
+    cudaEvent_t e0 = res().event(0), e1 = res().event(1);
     double best = 0.0;
     for (int rep = 0; rep < 5; ++rep) {
         cudaEventRecord(e0, st);

@@ -384,18 +384,45 @@ double ag_select_bench_ns(const ag_selector* s, int64_t m, int64_t n, int64_t k,
     return std::chrono::duration<double, std::nano>(t1 - t0).count() / (double)reps;
 }
 
+}  // extern "C"
+
+namespace ag {
+int set_last_error(int code, const std::string& msg);
+std::string config_string(const ag_config& c);
+}  // namespace ag
+
+namespace {
+// the tree's pick, or the fallback when the pick is illegal under `caps` or
+// has no compiled kernel for `dtype` (codegen.py:312-322 legality fallback)
+int pick_config(const ag_selector* sel, const ag_config* fallback, const ag_shape* shape, const ag_caps* caps,
+                int dtype, ag_config* pick, int* fb) {
+    if (!sel) return ag::set_last_error(AG_ERR_CONFIG, "null selector");
+    if (!shape) return ag::set_last_error(AG_ERR_SHAPE, "null shape");
+    *pick = sel->cfg[leaf_of(sel, shape->m, shape->n, shape->k)];
+    *fb = 0;
+    auto usable = [&](const ag_config* c) { return (!caps || ag_is_legal(c, caps)) && ag_has_kernel(c, dtype); };
+    if (usable(pick)) return AG_OK;
+    if (!fallback || !usable(fallback))
+        return ag::set_last_error(AG_ERR_CONFIG, "selected config " + ag::config_string(*pick) +
+                                                     " is not runnable and the fallback " +
+                                                     (fallback ? ag::config_string(*fallback) : std::string("(none)")) +
+                                                     " is not either");
+    *pick = *fallback;
+    *fb = 1;
+    return AG_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int ag_dispatch_gemm(const ag_selector* sel, const ag_config* fallback, const ag_shape* shape, const ag_caps* caps,
                      int dtype, const void* A, int64_t lda, const void* B, int64_t ldb, const void* C, int64_t ldc,
                      void* out, int64_t ldo, void* workspace, size_t workspace_bytes, void* stream,
                      ag_config* selected, int* used_fallback) {
-    if (!sel || !shape) return AG_ERR_CONFIG;
-    ag_config pick = sel->cfg[leaf_of(sel, shape->m, shape->n, shape->k)];
+    ag_config pick;
     int fb = 0;
-    if (caps && !ag_is_legal(&pick, caps)) {
-        if (!fallback || !ag_is_legal(fallback, caps)) return AG_ERR_CONFIG;
-        pick = *fallback;
-        fb = 1;
-    }
+    const int r = pick_config(sel, fallback, shape, caps, dtype, &pick, &fb);
+    if (r) return r;
     if (selected) *selected = pick;
     if (used_fallback) *used_fallback = fb;
     return ag_gemm(shape, &pick, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, workspace, workspace_bytes, stream);
@@ -405,18 +432,29 @@ int ag_dispatch_gemm_host(const ag_selector* sel, const ag_config* fallback, con
                           const ag_caps* caps, int dtype, const void* A, int64_t lda, const void* B, int64_t ldb,
                           const void* C, int64_t ldc, void* out, int64_t ldo, void* device_scratch,
                           size_t scratch_bytes, int panels, void* stream, ag_config* selected, int* used_fallback) {
-    if (!sel || !shape) return AG_ERR_CONFIG;
-    ag_config pick = sel->cfg[leaf_of(sel, shape->m, shape->n, shape->k)];
+    ag_config pick;
     int fb = 0;
-    if (caps && !ag_is_legal(&pick, caps)) {
-        if (!fallback || !ag_is_legal(fallback, caps)) return AG_ERR_CONFIG;
-        pick = *fallback;
-        fb = 1;
-    }
+    const int r = pick_config(sel, fallback, shape, caps, dtype, &pick, &fb);
+    if (r) return r;
     if (selected) *selected = pick;
     if (used_fallback) *used_fallback = fb;
     return ag_gemm_host(shape, &pick, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, device_scratch, scratch_bytes,
                         panels, stream);
+}
+
+int ag_dispatch_gemm_host_ex(const ag_selector* sel, const ag_config* fallback, const ag_shape* shape,
+                             const ag_caps* caps, int dtype, const void* A, int64_t lda, const void* B, int64_t ldb,
+                             const void* C, int64_t ldc, void* out, int64_t ldo, void* device_scratch,
+                             size_t scratch_bytes, int panels, int flags, void* stream, ag_config* selected,
+                             int* used_fallback, double* kernel_seconds) {
+    ag_config pick;
+    int fb = 0;
+    const int r = pick_config(sel, fallback, shape, caps, dtype, &pick, &fb);
+    if (r) return r;
+    if (selected) *selected = pick;
+    if (used_fallback) *used_fallback = fb;
+    return ag_gemm_host_ex(shape, &pick, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, device_scratch,
+                           scratch_bytes, panels, flags, stream, kernel_seconds);
 }
 
 }  // extern "C"

@@ -203,7 +203,7 @@ int launch_tma(const GemmCall& c) {
     constexpr size_t smem = smem_bytes<BM, BN, STAGES>();
     static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
     auto kernel = tma_gemm_kernel<BM, BN, TM, TN, STAGES>;
-    static std::atomic<size_t> granted{0};
+    static SmemGrant granted;
     if (ensure_smem(kernel, smem, granted) != cudaSuccess) return fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
     const i64 M = c.M, N = c.N, K = c.K;
     const i64 tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;

@@ -879,16 +879,18 @@ reference_gemm_kernel(int M, int N, int K, double alpha, double beta, int ta, in
                       const T* __restrict__ A, i64 lda, const T* __restrict__ B, i64 ldb,
                       const T* __restrict__ C, i64 ldc, T* __restrict__ out, i64 ldo) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i = blockIdx.y;
-    if (j >= N || i >= M) return;
-    double acc = 0.0;
-    for (int k = 0; k < K; ++k) {
-        const double a = (double)(ta ? A[(i64)k * lda + i] : A[(i64)i * lda + k]);
-        const double b = (double)(tb ? B[(i64)j * ldb + k] : B[(i64)k * ldb + j]);
-        acc = __dadd_rn(acc, __dmul_rn(a, b));
+    if (j >= N) return;
+    // rows strided over grid.y (<= 65535), so any M runs
+    for (int i = blockIdx.y; i < M; i += gridDim.y) {
+        double acc = 0.0;
+        for (int k = 0; k < K; ++k) {
+            const double a = (double)(ta ? A[(i64)k * lda + i] : A[(i64)i * lda + k]);
+            const double b = (double)(tb ? B[(i64)j * ldb + k] : B[(i64)k * ldb + j]);
+            acc = __dadd_rn(acc, __dmul_rn(a, b));
+        }
+        const double r = __dadd_rn(__dmul_rn(alpha, acc), __dmul_rn(beta, (double)C[(i64)i * ldc + j]));
+        out[(i64)i * ldo + j] = (T)r;
     }
-    const double r = __dadd_rn(__dmul_rn(alpha, acc), __dmul_rn(beta, (double)C[(i64)i * ldc + j]));
-    out[(i64)i * ldo + j] = (T)r;
 }
 
 }  // namespace ag

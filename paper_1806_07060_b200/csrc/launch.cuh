@@ -21,10 +21,42 @@ namespace ag {
 
 inline i64 round_up(i64 x, i64 s) { return (x + s - 1) / s * s; }
 
-// raise the per-kernel dynamic shared-memory limit once per needed size
+// Per-device one-shot state.  Kernel attributes (cudaFuncSetAttribute) and
+// device properties apply to the CURRENT device, so every cache below is
+// indexed by it: one process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    return dev;
+}
+template <typename T>
+struct PerDevice {
+    std::atomic<T> v[kMaxDevices];
+    PerDevice() {
+        for (auto& x : v) x.store(T(0));
+    }
+    std::atomic<T>& here() { return v[current_device()]; }
+};
+
+// SM count of the current device (grid sizing)
+inline int device_sms() {
+    static PerDevice<int> cache;
+    auto& slot = cache.here();
+    int n = slot.load(std::memory_order_relaxed);
+    if (n > 0) return n;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device()) != cudaSuccess || n <= 0) n = 148;
+    slot.store(n);
+    return n;
+}
+
+// raise the per-kernel dynamic shared-memory limit once per needed size and device
+using SmemGrant = PerDevice<size_t>;
 template <typename K>
-inline cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& granted) {
-    if (bytes <= 48 * 1024 || bytes <= granted.load(std::memory_order_relaxed)) return cudaSuccess;
+inline cudaError_t ensure_smem(K kernel, size_t bytes, SmemGrant& grants) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    std::atomic<size_t>& granted = grants.here();
+    if (bytes <= granted.load(std::memory_order_relaxed)) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e == cudaSuccess) {
         size_t cur = granted.load();
@@ -71,12 +103,7 @@ int launch_pack(T* dst, i64 ld_dst, i64 dst_rows, i64 dst_cols, const T* src, i6
     if (!transpose && dst_cols % W == 0 && ld_dst % W == 0 && aligned(dst, 16)) {
         const bool vec = ld_src % W == 0 && aligned(src, 16);
         const i64 total = dst_rows * (dst_cols / W);
-        static const int sms = [] {
-            int dev = 0, n = 148;
-            cudaGetDevice(&dev);
-            if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-            return n;
-        }();  // grid sizing only
+        const int sms = device_sms();  // grid sizing only
         const unsigned blocks = (unsigned)std::max<i64>(1, std::min<i64>((total + 1023) / 1024, (i64)sms * 8));
         if (vec)
             pack_copy_kernel<T, true><<<blocks, 256, 0, stream>>>(dst, ld_dst, (int)dst_rows, (int)dst_cols, src,
@@ -102,7 +129,7 @@ int launch_direct(const GemmCall& c) {
     const size_t smem = direct_smem_bytes<T>(bm, bn, bk);
     if (smem > 227 * 1024) return fail(c, AG_ERR_CONFIG, "config exceeds 227 KB shared memory per CTA");
     auto kernel = direct_gemm_kernel<T, BM, BN, BK, TM, TN>;
-    static std::atomic<size_t> granted{0};
+    static SmemGrant granted;
     if (ensure_smem(kernel, smem, granted) != cudaSuccess) return fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
     const i64 gy = (c.M + bm - 1) / bm, gx = (c.N + bn - 1) / bn;
     if (gy > 65535 || gx > 0x7fffffff) return fail(c, AG_ERR_SHAPE, "problem too large for the direct grid");
@@ -162,7 +189,7 @@ int launch_inplace(const GemmCall& c) {
     constexpr size_t smem = inplace_smem_bytes(BM, BN, BK);
     static_assert(smem <= 227 * 1024, "in-place stage ring exceeds shared memory");
     auto kernel = inplace_gemm_kernel<BM, BN, BK, TM, TN, STAGES>;
-    static std::atomic<size_t> granted{0};
+    static SmemGrant granted;
     if (ensure_smem(kernel, smem, granted) != cudaSuccess) return fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
     const i64 M = c.M, N = c.N, K = c.K;
     const i64 Mp = round_up(M, BM), Np = round_up(N, BN), Kp = round_up(K, BK);
@@ -200,7 +227,8 @@ int launch_inplace(const GemmCall& c) {
 #else
     if (used_splits > 1 && used_splits <= 16) {
 #endif
-        static std::atomic<int> np_ok{0};
+        static PerDevice<int> np_ok_dev;
+        std::atomic<int>& np_ok = np_ok_dev.here();
         if (used_splits > 8 && !np_ok.load()) {
             if (cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
                 np_ok.store(1);
@@ -230,7 +258,7 @@ int launch_inplace(const GemmCall& c) {
     if (cudaGetLastError() != cudaSuccess) return fail(c, AG_ERR_CUDA, "in-place kernel launch failed");
     if (used_splits > 1) {
         const i64 total = M * N;
-        const unsigned blocks = (unsigned)std::min<i64>((total + 255) / 256, 148 * 16);
+        const unsigned blocks = (unsigned)std::min<i64>((total + 255) / 256, (i64)device_sms() * 16);
         const cudaError_t le = launch_maybe_dependent(
             splitk_reduce_kernel<float>, dim3(blocks), dim3(256), 0, c.stream, true, (const float*)p.partial,
             used_splits, (i64)(Mp * Np), (int)Np, (int)M, (int)N, p.alpha, p.beta, p.use_c, p.C, (i64)c.ldc, p.out,
@@ -277,10 +305,10 @@ int launch_indirect(const GemmCall& c) {
                              : tiled_smem_bytes<T>(bm, bn, bk, STAGES);
     if (smem > 227 * 1024) return fail(c, AG_ERR_CONFIG, "config exceeds 227 KB shared memory per CTA");
     auto kernel = tiled_gemm_kernel<T, BM, BN, BK, TM, TN, UK, STAGES>;
-    static std::atomic<size_t> granted{0};
+    static SmemGrant granted;
     cudaError_t attr = cudaSuccess;
     if constexpr (AROW_OK && FIXED) {
-        static std::atomic<size_t> granted_arow{0};
+        static SmemGrant granted_arow;
         attr = arow ? ensure_smem(tiled_gemm_kernel<T, BM, BN, BK, TM, TN, UK, STAGES_AROW, true>, smem, granted_arow)
                     : ensure_smem(kernel, smem, granted);
     } else {
@@ -369,7 +397,7 @@ int launch_indirect(const GemmCall& c) {
         return fail(c, AG_ERR_CUDA, "indirect kernel launch failed");
     if (used_splits > 1) {
         const i64 total = M * N;
-        const unsigned blocks = (unsigned)std::min<i64>((total + 255) / 256, 148 * 16);
+        const unsigned blocks = (unsigned)std::min<i64>((total + 255) / 256, (i64)device_sms() * 16);
         le = launch_maybe_dependent(splitk_reduce_kernel<T>, dim3(blocks), dim3(256), 0, c.stream, true,
                                     (const T*)p.partial, used_splits, (i64)(Mp * Np), (int)Np, (int)M, (int)N,
                                     p.alpha, p.beta, p.use_c, p.C, (i64)c.ldc, p.out, (i64)c.ldo);

@@ -39,6 +39,7 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 #include "registry.h"
 
 namespace ag {
@@ -622,16 +623,7 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-inline int sm_count() {
-    static int n = 0;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-    });
-    return n;
-}
+inline int sm_count() { return device_sms(); }  // per device (launch.cuh)
 
 // One operand as stored: `rows` x `cols` row-major with leading dimension
 // `ld` (elements of the MMA type).  K-major when the contiguous dimension is
@@ -784,12 +776,9 @@ int launch_tc(const GemmCall& c) {
     const size_t smem = std::max<size_t>(smem_bytes<BN, STAGES, CTAS>(), 116 * 1024);
     if (smem > 227 * 1024) return tc_fail(c, AG_ERR_CONFIG, "config exceeds 227 KB shared memory per CTA");
     auto kernel = tc_gemm_kernel<KIND, BN, STAGES, CTAS>;
-    static std::atomic<int> attr_done{0};
-    if (!attr_done.load()) {
-        if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return tc_fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
-        attr_done.store(1);
-    }
+    static SmemGrant granted;  // per device: the attribute applies to the current device only
+    if (ensure_smem(kernel, smem, granted) != cudaSuccess)
+        return tc_fail(c, AG_ERR_CUDA, "cudaFuncSetAttribute failed");
     // persistent: one CTA (pair) per SM (TPC), tiles strided over units
     const i64 units = std::min<i64>(tiles_m * tiles_n, sm_count() / CTAS);
     cudaLaunchConfig_t cfg = {};

@@ -461,8 +461,9 @@ def gemm_reference(shape: ProblemShape, A, B, C, out=None):
     ops = _Operands(shape, A, B, C, out)
     lib = _native.lib()
     a, lda, b, ldb, c, ldc, o, ldo = ops.args()
-    rc = lib.ag_gemm_reference(ctypes.byref(native_shape(shape)), ops.code, a, lda, b, ldb, c, ldc,
-                               o, ldo, ctypes.c_void_p(_device.current_stream_handle(ops.device)))
+    with _device.guard(ops.device):
+        rc = lib.ag_gemm_reference(ctypes.byref(native_shape(shape)), ops.code, a, lda, b, ldb, c, ldc,
+                                   o, ldo, ctypes.c_void_p(_device.current_stream_handle(ops.device)))
     if rc:
         _raise_for(rc)
     return ops.result()
@@ -485,9 +486,10 @@ def pack_padded(X, rows: int, cols: int, transpose: bool, pad_rows: int, pad_col
     if _dims(src) != want:
         raise ShapeError(f"X has shape {_dims(src)}, expected {want}")
     dst = t.empty((pad_rows, pad_cols), dtype=src.dtype, device=dev)
-    rc = _native.lib().ag_pack_padded(code, ctypes.c_void_p(src.data_ptr()), _device.leading_dim(src),
-                                      rows, cols, int(bool(transpose)), ctypes.c_void_p(dst.data_ptr()),
-                                      pad_rows, pad_cols, ctypes.c_void_p(_device.current_stream_handle(dev)))
+    with _device.guard(dev):
+        rc = _native.lib().ag_pack_padded(code, ctypes.c_void_p(src.data_ptr()), _device.leading_dim(src),
+                                          rows, cols, int(bool(transpose)), ctypes.c_void_p(dst.data_ptr()),
+                                          pad_rows, pad_cols, ctypes.c_void_p(_device.current_stream_handle(dev)))
     if rc:
         _raise_for(rc)
     return dst.cpu().numpy() if host else dst
@@ -495,13 +497,18 @@ def pack_padded(X, rows: int, cols: int, transpose: bool, pad_rows: int, pad_col
 
 def _launch(shape: ProblemShape, config: KernelConfig, caps: DeviceCaps, ops: _Operands,
             timed: bool) -> float:
+    with _device.guard(ops.device):
+        return _launch_here(shape, config, caps, ops, timed)
+
+
+def _launch_here(shape, config, caps, ops, timed):
     t = _device.torch()
     lib = _native.lib()
     nshape, ncfg, ncaps = native_shape(shape), config.native(), caps.native()
     ws_n = int(lib.ag_workspace_bytes(ctypes.byref(nshape), ctypes.byref(ncfg), ops.code))
-    ws = _device.workspace(ws_n, ops.device) if ws_n else None
-    ws_ptr = ctypes.c_void_p(ws.data_ptr() if ws is not None else 0)
     stream = t.cuda.current_stream(ops.device)
+    ws = _device.workspace(ws_n, ops.device, stream.cuda_stream) if ws_n else None
+    ws_ptr = ctypes.c_void_p(ws.data_ptr() if ws is not None else 0)
     a, lda, b, ldb, c, ldc, o, ldo = ops.args()
     if timed:
         e0 = t.cuda.Event(enable_timing=True)

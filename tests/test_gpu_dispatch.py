@@ -108,10 +108,10 @@ def test_cli_tune_sharded_workers(tmp_path, capsys):
     from paper_1806_07060_b200.cli import main
     out = tmp_path / "par"
     cfg = _config(tmp_path, out, caps={"profile": "b200"})
-    assert main(["tune", "--config", str(cfg), "--gpus", "2"]) == 0
+    assert main(["tune", "--config", str(cfg), "--gpus", "2", "--share-gpus"]) == 0
     tables = sorted(p.name for p in (out / "tables").glob("*.csv"))
     assert tables == ["16x16x16.csv", "24x24x24.csv", "32x32x32.csv", "8x8x8.csv"]
-    assert main(["tune", "--config", str(cfg), "--gpus", "2", "--force"]) == 0
+    assert main(["tune", "--config", str(cfg), "--gpus", "2", "--share-gpus", "--force"]) == 0
     assert "0 already done, 4 to run" in capsys.readouterr().out
 
 
@@ -211,3 +211,59 @@ def test_host_path_random_shapes_and_panels():
         ref, _, _ = codegen.dispatch_native(sel, s, dA, dB, dC, caps)
         got, _, _ = codegen.dispatch_native(sel, s, A, B, C, caps, panels=1 + stream.below(5))
         np.testing.assert_array_equal(got, ref.cpu().numpy(), err_msg=f"{s} {cfg.canonical()}")
+
+
+def test_acceptance_c11_pipeline_on_gpu(tmp_path, capsys):
+    """The reference's acceptance criterion 11 (test_acceptance.py:339-387)
+    on the B200: the 27-shape po2(64, 256) pipeline from one config file,
+    tune -> dataset -> train -> eval -> codegen -> bench, the model's train
+    DTPR >= the baseline's, within the reference's 1800 s bound (the CPU
+    reference took 862 s)."""
+    import json
+    import time
+
+    from paper_1806_07060_b200 import evaluation
+    from paper_1806_07060_b200.cli import main
+    from paper_1806_07060_b200.dataset import load_dataset, split
+    from paper_1806_07060_b200.model import load_tree
+    from paper_1806_07060_b200.tuner import load_table, table_filename
+
+    started = time.monotonic()
+    out = tmp_path / "run"
+    config = {
+        "out_dir": str(out),
+        "timing": {"warmup": 1, "repeats": 3},
+        "dataset": {"strategy": "po2", "min": 64, "max": 256},
+        "split": {"fraction": 0.8, "seed": 20817},
+        "baseline": {"threshold": 384, "direct_anchor": [64, 64, 64], "indirect_anchor": [256, 256, 256]},
+    }
+    cfg_path = tmp_path / "smoke.json"
+    cfg_path.write_text(json.dumps(config, indent=1))
+    stage_s = {}
+    for stage in ("tune", "dataset", "train", "eval", "codegen", "bench"):
+        t0 = time.monotonic()
+        assert main([stage, "--config", str(cfg_path)]) == 0, stage
+        stage_s[stage] = round(time.monotonic() - t0, 2)
+    ds = load_dataset(out / "dataset.csv", out / "dataset_classes.json")
+    assert len(ds.records) == 27
+    sp = split(ds, 0.8, seed=20817)
+    records = ds.features_and_labels()
+    train_records = [records[i] for i in sp.train]
+    tables = evaluation.tables_by_shape([load_table(out / "tables" / table_filename(r.input)) for r in ds.records])
+    best_name = json.loads((out / "best_model.json").read_text())["name"]
+    best_tree = load_tree(out / "models" / f"{best_name}.json")
+    base_doc = json.loads((out / "baseline.json").read_text())
+    policy = evaluation.BaselinePolicy(
+        default_indirect=KernelConfig.from_canonical(base_doc["default_indirect"]),
+        default_direct=KernelConfig.from_canonical(base_doc["default_direct"]),
+        threshold=base_doc["threshold"]).register(ds.class_index)
+    model_dtpr = evaluation.dtpr(best_tree, train_records, tables, ds.class_index)
+    base_preds = [evaluation.baseline_select(policy, ds.records[i].input) for i in sp.train]
+    base_dtpr = evaluation.dtpr_from_predictions(base_preds, train_records, tables, ds.class_index)
+    assert model_dtpr >= base_dtpr
+    assert (out / "dispatcher.c").exists() and (out / "dispatcher.py").exists()
+    elapsed = time.monotonic() - started
+    with capsys.disabled():
+        print(f"\n[acceptance C11 on B200] {elapsed:.1f} s (CPU reference 862 s); stages {stage_s}; "
+              f"best={best_name} train-dtpr={model_dtpr:.4f} baseline-dtpr={base_dtpr:.4f}")
+    assert elapsed < 1800.0

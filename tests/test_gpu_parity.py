@@ -406,3 +406,36 @@ def test_tma_family_fallbacks():
     A, B, C = rand_operands(s, np.float64, seed=6)
     out, _ = gemm_execute(s, cfg, A, B, C, B200)
     assert out.dtype == np.float64 and rel_frobenius(out, _oracle_ref(s, A, B, C)) <= 1e-12
+
+
+def test_every_b200_fp32_family_config_runs_float64():
+    """Legality is dtype-independent (kernels.py:145-158): every config of the
+    B200 profile's CUDA-core families runs float64 operands (run-time-tile
+    kernels; a larger register tile when the float64 CTA would exceed the
+    kernel's thread bound) at the float64 bar."""
+    from paper_1806_07060_b200.kernels import full_search_space
+    s = ProblemShape(67, 45, 33, alpha=1.5, beta=0.5)
+    A, B, C = rand_operands(s, np.float64, seed=41)
+    ref = _oracle_ref(s, A, B, C)
+    bad = []
+    for cfg in full_search_space(B200):
+        out, _ = gemm_execute(s, cfg, A, B, C, B200)
+        if rel_frobenius(out, ref) > 1e-12:
+            bad.append(cfg.canonical())
+    assert not bad, bad[:10]
+
+
+def test_tc_config_on_float64_falls_back_in_dispatch():
+    """The tf32/bf16 families have no float64 kernels: gemm_execute raises
+    ConfigError, and the native dispatch takes the fallback config."""
+    from paper_1806_07060_b200 import codegen, model
+    s = ProblemShape(40, 30, 20)
+    A, B, C = rand_operands(s, np.float64, seed=42)
+    tc = KernelConfig.from_canonical("bf16:128-128-64-4-1-1")
+    with pytest.raises(ConfigError):
+        gemm_execute(s, tc, A, B, C, DeviceCaps.b200_tc())
+    tree = model.train([((40, 30, 20), 0)])
+    sel = codegen.CompiledSelector(tree, {0: tc})
+    out, picked, fb = codegen.dispatch_native(sel, s, A, B, C, DeviceCaps.b200_tc())
+    assert fb and picked == codegen.FALLBACK_CONFIG
+    assert rel_frobenius(out, _oracle_ref(s, A, B, C)) <= 1e-12

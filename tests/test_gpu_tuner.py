@@ -87,3 +87,29 @@ def test_timing_repeatability():
     b = time_configs(s, cfg, DeviceCaps(), TimingPolicy(2, 7), bufs)
     for x, y in zip(a, b):
         assert abs(x - y) / min(x, y) < 0.25
+
+
+@pytest.mark.parametrize("profile", ["b200", "b200_tc"])
+def test_tune_random_b200_profiles(profile):
+    """tune_random (tuner.py:188-221) over the enlarged B200 spaces: the
+    seeded sample is the host-side sampler's, allocated per family by
+    largest remainder, every pick legal and timed on the device."""
+    from paper_1806_07060_b200.kernels import enumerate_search_space, full_search_space
+    from paper_1806_07060_b200.tuner import random_configs
+
+    caps = getattr(DeviceCaps, profile)()
+    s = ProblemShape(300, 200, 500)
+    samples, seed = 64, 1806
+    t = tune_random(s, caps, samples=samples, seed=seed, timing=FAST)
+    picked = [m.config for m in t.measurements]
+    assert picked == random_configs(caps, samples, seed)
+    assert len(set(picked)) == samples and all(is_legal(c, caps) for c in picked)
+    assert all(m.gflops > 0 for m in t.measurements) and t.best_config in picked
+    total = len(full_search_space(caps))
+    for fam in KernelFamily:
+        size = len(enumerate_search_space(fam, caps))
+        got = sum(1 for c in picked if c.family is fam)
+        exact = samples * size / total
+        assert int(exact) <= got <= int(exact) + 1, (fam, got, exact)
+    again = tune_random(s, caps, samples=samples, seed=seed, timing=FAST)
+    assert [m.config for m in again.measurements] == picked
