@@ -265,6 +265,9 @@ def pack_launches(shape, cfg) -> int:
     from paper_1806_07060_b200.kernels import TC_FAMILIES, KernelFamily
     if cfg.family is KernelFamily.DIRECT:
         return 1
+    if cfg.family in (KernelFamily.SKINNY_N, KernelFamily.SKINNY_M) and not shape.transA and not shape.transB \
+            and shape.K % 4 == 0 and (cfg.family is KernelFamily.SKINNY_M or shape.N % 4 == 0):
+        return 1  # one clustered launch (skinny.cuh)
     if cfg.family in TC_FAMILIES:  # bf16: one convert pass per operand; tf32 reads fp32 in place
         return 3 if cfg.family is KernelFamily.BF16 else 1
     if cfg.family is KernelFamily.TMA and not shape.transA and not shape.transB and shape.K % 4 == 0 \

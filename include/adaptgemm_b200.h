@@ -57,6 +57,17 @@ extern "C" {
  * operands (no pack passes; transposed / unaligned operands run the packed
  * core with the same tile and the same bits) */
 #define AG_FAMILY_TMA 5
+/* B200 profiles, the "skinny" families (csrc/skinny.cuh): streaming
+ * kernels for one small output side, K split over `uk` CTAs of one cluster
+ * (DSMEM reduction in a fixed order).
+ *   skinny_n (N small): bm = 32 * tm rows per CTA, bn = N tile (16/32/64),
+ *     bk = 32, tm = rows per thread, tn = warps splitting the CTA's K range,
+ *     uk = K slices (CTAs per cluster).
+ *   skinny_m (M small): bm = M tile (8..64), bn = CTA columns
+ *     (= 32 * warps * tn), bk = 32, tm = 1, tn = columns per thread, uk =
+ *     K slices. */
+#define AG_FAMILY_SKINNY_N 6
+#define AG_FAMILY_SKINNY_M 7
 
 /* element types accepted by gemm_execute (kernels.py:282-283) */
 #define AG_F32 0

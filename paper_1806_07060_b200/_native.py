@@ -17,6 +17,7 @@ AG_HOST_REGISTER = 1  # ag_gemm_host_ex flag: page-lock the caller's host buffer
 AG_FAMILY_DIRECT, AG_FAMILY_INDIRECT, AG_FAMILY_SPLITK = 0, 1, 2
 AG_FAMILY_TF32, AG_FAMILY_BF16 = 3, 4
 AG_FAMILY_TMA = 5
+AG_FAMILY_SKINNY_N, AG_FAMILY_SKINNY_M = 6, 7
 AG_F32, AG_F64 = 0, 1
 
 

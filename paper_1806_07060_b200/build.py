@@ -41,7 +41,7 @@ CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-O2", "-fPIC", "-std=c++17", "-Wall", f"-I{INCLUDE}"]
 
 N_UNITS = 48
-FAMILY_CODE = {"direct": 0, "indirect": 1, "splitk": 2, "tf32": 3, "bf16": 4, "tma": 5}
+FAMILY_CODE = {"direct": 0, "indirect": 1, "splitk": 2, "tf32": 3, "bf16": 4, "tma": 5, "skinny_n": 6, "skinny_m": 7}
 
 
 def _cost(t):
@@ -72,6 +72,17 @@ def kernel_entries():
     for bm, bn, tm, tn in spaces.TMA_TILES:
         out.append((5, 0, bm, bn, spaces.TMA_BLOCK_K, tm, tn, 1,
                     f"&ag::f32tma::launch_tma_family<{bm}, {bn}, {tm}, {tn}>", 2.0 + tm * tn * 32 / 64.0))
+    # skinny families (csrc/skinny.cuh): one kernel per tile; the K slice
+    # count is a run-time argument (key uk = 0)
+    for tm, bn in spaces.SKINNY_N_TILES:
+        for w in spaces.SKINNY_N_WARPS:
+            if spaces.is_legal_tuple("skinny_n", 32 * tm, bn, spaces.SKINNY_BLOCK_K, tm, w, 1, spaces.B200_CAPS):
+                out.append((6, 0, 32 * tm, bn, spaces.SKINNY_BLOCK_K, tm, w, 0,
+                            f"&ag::skinny::launch_n<{tm}, {bn}, {w}>", 3.0 + tm * bn / 16.0))
+    for bm, tn in spaces.SKINNY_M_TILES:
+        for w in spaces.SKINNY_M_WARPS:
+            out.append((7, 0, bm, 32 * w * tn, spaces.SKINNY_BLOCK_K, 1, tn, 0,
+                        f"&ag::skinny::launch_m<{bm}, {tn}, {w}>", 3.0 + bm * tn / 16.0))
     # tensor-core families: one persistent tcgen05 kernel per (kind, bn, stages)
     for fam in spaces.TC_FAMILIES:
         for t in spaces.enumerate_tuples(fam, spaces.B200_CAPS, spaces.PROFILE_B200_TC):
@@ -113,7 +124,8 @@ def generate():
     for u, ents in enumerate(units):
         ents.sort(key=lambda e: e[:8])
         lines = ["// generated by paper_1806_07060_b200/build.py -- do not edit",
-                 '#include "../launch.cuh"', '#include "../tc_kernels.cuh"', '#include "../fp32_tma.cuh"', "", "namespace {",
+                 '#include "../launch.cuh"', '#include "../tc_kernels.cuh"', '#include "../fp32_tma.cuh"',
+                 '#include "../skinny.cuh"', "", "namespace {",
                  "const ag::KernelEntry kEntries[] = {"]
         for fam, dt, bm, bn, bk, tm, tn, uk, fn, _ in ents:
             lines.append(f"    {{{fam}, {dt}, {bm}, {bn}, {bk}, {tm}, {tn}, {uk}, {fn}}},")

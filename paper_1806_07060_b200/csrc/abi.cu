@@ -18,6 +18,7 @@
 #include "kernels.cuh"
 #include "launch.cuh"
 #include "registry.h"
+#include "skinny.cuh"
 #include "tc_kernels.cuh"
 
 extern const ag::EntryTableFn g_entry_tables[];
@@ -112,6 +113,11 @@ ag::LaunchFn find_kernel(const ag_config& c, int dtype) {
         if (it != m.end()) return it->second;
         return find_runtime(c, AG_FAMILY_INDIRECT, dtype);
     }
+    if (c.family == AG_FAMILY_SKINNY_N || c.family == AG_FAMILY_SKINNY_M) {  // one launcher for both dtypes:
+        // float64 (and calls the kernels cannot take) run its split-K fallback
+        auto it = m.find(make_key(c.family, AG_F32, c.bm, c.bn, c.bk, c.tm, c.tn, 0));
+        return it != m.end() ? it->second : nullptr;
+    }
     if (c.family == AG_FAMILY_TMA) {  // float32: its own launcher; float64: the indirect run-time-tile kernel
         auto it = m.find(make_key(AG_FAMILY_TMA, dtype, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk));
         if (it != m.end()) return it->second;
@@ -129,6 +135,8 @@ std::string config_str(const ag_config& c) {
                       : c.family == AG_FAMILY_TF32   ? "tf32"
                       : c.family == AG_FAMILY_BF16   ? "bf16"
                       : c.family == AG_FAMILY_TMA    ? "tma"
+                      : c.family == AG_FAMILY_SKINNY_N ? "skinny_n"
+                      : c.family == AG_FAMILY_SKINNY_M ? "skinny_m"
                                                      : "indirect";
     snprintf(buf, sizeof buf, "%s:%d-%d-%d-%d-%d-%d", fam, c.bm, c.bn, c.bk, c.tm, c.tn, c.uk);
     return buf;
@@ -161,7 +169,8 @@ ag::GemmCall make_call(const ag_shape* s, const ag_config* c, int dtype, const v
     g.stream = static_cast<cudaStream_t>(stream);
     g.bm = c->bm; g.bn = c->bn; g.bk = c->bk; g.tm = c->tm; g.tn = c->tn; g.uk = c->uk;
     g.splits = 1;
-    if (c->family == AG_FAMILY_SPLITK) {  // unroll_k carries the number of K slices
+    if (c->family == AG_FAMILY_SPLITK || c->family == AG_FAMILY_SKINNY_N ||
+        c->family == AG_FAMILY_SKINNY_M) {  // unroll_k carries the number of K slices
         g.splits = c->uk;
         g.uk = 1;
     }
@@ -475,6 +484,25 @@ int ag_is_legal(const ag_config* c, const ag_caps* caps) {
         const int64_t smem = (int64_t)c->tm * (128 + c->bn / ctas) * 128 + 1024 + (int64_t)ag::tc::EPI_BYTES + 256;
         return smem <= 227 * 1024;
     }
+    if (c->family == AG_FAMILY_SKINNY_N || c->family == AG_FAMILY_SKINNY_M) {
+        // spaces.is_legal_tuple: the explicit skinny tile lists
+        static const int n_tiles[][2] = {{1, 16}, {2, 16}, {4, 16}, {1, 32}, {2, 32}, {1, 64}};
+        static const int m_tiles[][2] = {{8, 2}, {8, 4}, {16, 2}, {16, 4}, {24, 2}, {32, 2}, {40, 2}, {48, 2}};
+        const bool slices_ok = c->uk == 1 || c->uk == 2 || c->uk == 3 || c->uk == 4 || c->uk == 6 || c->uk == 8 ||
+                               c->uk == 12 || c->uk == 16;
+        if (c->bk != 32 || !slices_ok) return 0;
+        if (c->family == AG_FAMILY_SKINNY_N) {
+            bool tile = false;
+            for (const auto& t : n_tiles) tile = tile || (c->tm == t[0] && c->bn == t[1]);
+            return tile && c->bm == 32 * c->tm && (c->tn == 4 || c->tn == 8) &&
+                   (int64_t)c->tn * (4096 * c->tm + 128 * c->bn) <= 110 * 1024;
+        }
+        bool tile = false;
+        for (const auto& t : m_tiles) tile = tile || (c->bm == t[0] && c->tn == t[1]);
+        if (!tile || c->tm != 1 || c->bn % (32 * c->tn)) return 0;
+        const int warps = c->bn / (32 * c->tn);
+        return warps == 4 || warps == 8;
+    }
     if (c->family != AG_FAMILY_DIRECT && c->family != AG_FAMILY_INDIRECT && c->family != AG_FAMILY_SPLITK &&
         c->family != AG_FAMILY_TMA)
         return 0;
@@ -508,6 +536,12 @@ size_t ag_workspace_bytes(const ag_shape* s, const ag_config* c, int dtype) {
     if (!s || !c || c->family == AG_FAMILY_DIRECT || !in_range(*c)) return 0;
     if (c->family == AG_FAMILY_TF32) return ag::tc::workspace_bytes<ag::tc::KIND_TF32>(s->m, s->n, s->k, s->trans_a, s->trans_b);
     if (c->family == AG_FAMILY_BF16) return ag::tc::workspace_bytes<ag::tc::KIND_BF16>(s->m, s->n, s->k, s->trans_a, s->trans_b);
+    if (c->family == AG_FAMILY_SKINNY_N || c->family == AG_FAMILY_SKINNY_M) {
+        // no workspace on the skinny kernels; sized for their split-K fallback
+        // (transposed / unaligned / float64 calls: skinny.cuh fallback())
+        if (dtype == AG_F64) return ag::indirect_workspace_bytes<double>(s->m, s->n, s->k, 64, 64, 16, c->uk);
+        return ag::indirect_workspace_bytes<float>(s->m, s->n, s->k, 64, 64, 16, c->uk);
+    }
     const int splits = c->family == AG_FAMILY_SPLITK ? c->uk : 1;
     if (dtype == AG_F64) return ag::indirect_workspace_bytes<double>(s->m, s->n, s->k, c->bm, c->bn, c->bk, splits);
     return ag::indirect_workspace_bytes<float>(s->m, s->n, s->k, c->bm, c->bn, c->bk, splits);

@@ -45,6 +45,9 @@ class KernelFamily(str, Enum):
     or bf16, fp32 accumulation; they exist only in the "b200tc" profile.
     TMA is the indirect core's fp32 arithmetic fed by TMA from the caller's
     row-major operands (no pack passes; B200 profiles only).
+    SKINNY_N / SKINNY_M stream the big operand of a GEMM whose N (resp. M)
+    is small, K split over the CTAs of a cluster (csrc/skinny.cuh; B200
+    profiles only).
     Reference-profile spaces, tables and dispatchers are unchanged.
     """
 
@@ -54,6 +57,8 @@ class KernelFamily(str, Enum):
     TF32 = "tf32"
     BF16 = "bf16"
     TMA = "tma"
+    SKINNY_N = "skinny_n"
+    SKINNY_M = "skinny_m"
 
 
 TC_FAMILIES = (KernelFamily.TF32, KernelFamily.BF16)
@@ -65,7 +70,9 @@ _FAMILY_CODE = {KernelFamily.DIRECT: _native.AG_FAMILY_DIRECT,
                 KernelFamily.SPLITK: _native.AG_FAMILY_SPLITK,
                 KernelFamily.TF32: _native.AG_FAMILY_TF32,
                 KernelFamily.BF16: _native.AG_FAMILY_BF16,
-                KernelFamily.TMA: _native.AG_FAMILY_TMA}
+                KernelFamily.TMA: _native.AG_FAMILY_TMA,
+                KernelFamily.SKINNY_N: _native.AG_FAMILY_SKINNY_N,
+                KernelFamily.SKINNY_M: _native.AG_FAMILY_SKINNY_M}
 _CODE_FAMILY = {v: k for k, v in _FAMILY_CODE.items()}
 
 
@@ -226,6 +233,10 @@ def domains_for(family: KernelFamily) -> dict[str, tuple[int, ...]]:
                 "tile_m": tuple(sorted({t[2] for t in spaces.TMA_TILES})),
                 "tile_n": tuple(sorted({t[3] for t in spaces.TMA_TILES})),
                 "unroll_k": (1,)}
+    if family in (KernelFamily.SKINNY_N, KernelFamily.SKINNY_M):
+        tuples = spaces.enumerate_tuples(family.value, spaces.B200_CAPS, spaces.PROFILE_B200)
+        return {f: tuple(sorted({t[1 + i] for t in tuples})) for i, f in enumerate(
+            ("block_m", "block_n", "block_k", "tile_m", "tile_n", "unroll_k"))}
     return DIRECT_DOMAINS if family is KernelFamily.DIRECT else INDIRECT_DOMAINS
 
 

@@ -83,7 +83,19 @@ TC_SMEM_LIMIT = 227 * 1024
 TMA_TILES = ((128, 128, 8, 8), (128, 64, 8, 8), (64, 128, 8, 8), (64, 64, 8, 8), (64, 64, 8, 4),
              (64, 64, 4, 8), (64, 32, 8, 4), (32, 64, 4, 8))
 TMA_BLOCK_K = 32
-FAMILIES = ("direct", "indirect", "splitk") + TC_FAMILIES + ("tma",)
+# B200 profiles, skinny families (csrc/skinny.cuh), K over `uk` cluster slices.
+# skinny_n (N small): (tm, bn) register tiles (tm rows x all bn columns per
+# thread); bm = 32 tm rows per CTA; tn = warps splitting the CTA's K range.
+SKINNY_N_TILES = ((1, 16), (2, 16), (4, 16), (1, 32), (2, 32), (1, 64))
+SKINNY_N_WARPS = (4, 8)
+# skinny_m (M small): bm = M tile, tn = columns per thread (pairs for FFMA2),
+# warps per CTA; bn = 32 * warps * tn; accumulators bm * tn <= 96.
+SKINNY_M_TILES = ((8, 2), (8, 4), (16, 2), (16, 4), (24, 2), (32, 2), (40, 2), (48, 2))
+SKINNY_M_WARPS = (4, 8)
+SKINNY_SLICES = (1, 2, 3, 4, 6, 8, 12, 16)  # cluster sizes > 8 are non-portable
+SKINNY_BLOCK_K = 32
+SKINNY_FAMILIES = ("skinny_n", "skinny_m")
+FAMILIES = ("direct", "indirect", "splitk") + TC_FAMILIES + ("tma",) + SKINNY_FAMILIES
 
 PROFILE_REFERENCE = "reference"
 PROFILE_B200 = "b200"
@@ -142,6 +154,15 @@ def is_legal_tuple(family, bm, bn, bk, tm, tn, uk, caps) -> bool:
         return tc_smem_bytes(bm, bn, tm) <= TC_SMEM_LIMIT
     if family == "direct" and uk != 1:
         return False
+    if family == "skinny_n":
+        if (tm, bn) not in SKINNY_N_TILES or bm != 32 * tm or bk != SKINNY_BLOCK_K:
+            return False
+        # a 2-deep TMA ring per warp fits one CTA's shared memory
+        return tn in SKINNY_N_WARPS and uk in SKINNY_SLICES and tn * (4096 * tm + 128 * bn) <= 110 * 1024
+    if family == "skinny_m":
+        if (bm, tn) not in SKINNY_M_TILES or tm != 1 or bk != SKINNY_BLOCK_K or bn % (32 * tn):
+            return False
+        return bn // (32 * tn) in SKINNY_M_WARPS and uk in SKINNY_SLICES
     if family == "tma":
         # one 128-byte A row per k block, boxes of at most 256 rows, whole warps
         if bk != TMA_BLOCK_K or uk != 1 or bm > 256 or bn > 256 or bn % 4:
@@ -185,6 +206,16 @@ def enumerate_tuples(family, caps, profile=PROFILE_REFERENCE):
             return []
         return [t for (bm, bn, tm, tn) in TMA_TILES
                 for t in [("tma", bm, bn, TMA_BLOCK_K, tm, tn, 1)] if is_legal_tuple(*t, caps)]
+    if family == "skinny_n":
+        if not is_b200_profile(profile):
+            return []
+        return [t for (tm, bn) in SKINNY_N_TILES for w in SKINNY_N_WARPS for s in SKINNY_SLICES
+                for t in [("skinny_n", 32 * tm, bn, SKINNY_BLOCK_K, tm, w, s)] if is_legal_tuple(*t, caps)]
+    if family == "skinny_m":
+        if not is_b200_profile(profile):
+            return []
+        return [t for (bm, tn) in SKINNY_M_TILES for w in SKINNY_M_WARPS for s in SKINNY_SLICES
+                for t in [("skinny_m", bm, 32 * w * tn, SKINNY_BLOCK_K, 1, tn, s)] if is_legal_tuple(*t, caps)]
     if family == "splitk":
         if not is_b200_profile(profile):
             return []

@@ -439,3 +439,58 @@ def test_tc_config_on_float64_falls_back_in_dispatch():
     out, picked, fb = codegen.dispatch_native(sel, s, A, B, C, DeviceCaps.b200_tc())
     assert fb and picked == codegen.FALLBACK_CONFIG
     assert rel_frobenius(out, _oracle_ref(s, A, B, C)) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# skinny families (csrc/skinny.cuh, B200 profile)
+
+
+@pytest.mark.parametrize("family,mnk", [
+    ("skinny_n", (300, 16, 517)), ("skinny_n", (97, 40, 96)), ("skinny_n", (1000, 64, 1000)),
+    ("skinny_m", (35, 700, 517)), ("skinny_m", (9, 333, 96)), ("skinny_m", (64, 1001, 300)),
+])
+def test_skinny_every_config(family, mnk):
+    """Every config of the family on ragged shapes (M, N not tile multiples,
+    K not a multiple of 32, N odd for skinny_m), alpha / beta with C read:
+    RF <= 1e-5 vs the fp64 reference, and bitwise repeatable (fixed-order
+    cluster reduction)."""
+    from paper_1806_07060_b200.kernels import enumerate_search_space
+    s = ProblemShape(*mnk, alpha=1.25, beta=0.5)
+    A, B, C = rand_operands(s, seed=51)
+    ref = _oracle_ref(s, A, B, C)
+    fam = KernelFamily(family)
+    cfgs = enumerate_search_space(fam, B200)
+    assert cfgs
+    for cfg in cfgs:
+        out1, _ = gemm_execute(s, cfg, A, B, C, B200)
+        assert rel_frobenius(out1, ref) <= 1e-5, cfg.canonical()
+    for cfg in cfgs[::7]:
+        out1, _ = gemm_execute(s, cfg, A, B, C, B200)
+        out2, _ = gemm_execute(s, cfg, A, B, C, B200)
+        np.testing.assert_array_equal(out1, out2)
+
+
+@pytest.mark.parametrize("ta,tb", list(itertools.product([False, True], repeat=2)))
+def test_skinny_fallback_paths(ta, tb):
+    """Transposed operands, unaligned rows and float64 run the families'
+    split-K fallback at the same bars."""
+    for canon in ("skinny_n:64-16-32-2-4-4", "skinny_m:40-256-32-1-2-8"):
+        cfg = KernelConfig.from_canonical(canon)
+        for dt, bar in ((np.float32, 1e-5), (np.float64, 1e-12)):
+            s = ProblemShape(45, 37, 203, alpha=0.75, beta=0.25, transA=ta, transB=tb)  # K % 4 != 0
+            A, B, C = rand_operands(s, dt, seed=52)
+            out, _ = gemm_execute(s, cfg, A, B, C, B200)
+            assert rel_frobenius(out, _oracle_ref(s, A, B, C)) <= bar, (canon, dt)
+
+
+def test_skinny_full_size_deepbench():
+    import torch
+    for mnk, canon in (((4096, 16, 4096), "skinny_n:64-16-32-2-4-4"), ((7680, 16, 2560), "skinny_n:64-16-32-2-4-2"),
+                       ((35, 8457, 2560), "skinny_m:40-256-32-1-2-16"), ((35, 700, 2048), "skinny_m:16-256-32-1-2-16")):
+        s = ProblemShape(*mnk)
+        A, B, C = rand_operands(s, seed=53)
+        dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+        exact = dA.double() @ dB.double()
+        out, _ = gemm_execute(s, KernelConfig.from_canonical(canon), dA, dB, dC, B200)
+        rf = float(torch.linalg.norm(out.double() - exact) / torch.linalg.norm(exact))
+        assert rf <= 1e-5, (mnk, canon, rf)

@@ -73,7 +73,7 @@ def test_b200_profile_sweep_and_perf_floor():
     caps = DeviceCaps.b200()
     s = ProblemShape(2048, 2048, 2048)
     t = tune_exhaustive(s, caps, TimingPolicy(1, 3))
-    assert len(t.measurements) == 144 + 626 + 120 + 8  # direct + indirect + split-K + tma
+    assert len(t.measurements) == 144 + 626 + 120 + 8 + 88 + 128  # direct + indirect + split-K + tma + skinny_n + skinny_m
     # a big square must reach a large fraction of the FP32 FFMA peak
     assert t.peak_gflops > 35000, t.best_config.canonical()
     assert t.best_config.family is KernelFamily.INDIRECT
