@@ -212,10 +212,35 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = True) ->
         if res.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
         os.replace(tmp, LIB)
+    build_fastpath(force)
     if verbose:
         print(f"libadaptgemm_b200.so: {n} kernel instantiations, {compiled} units rebuilt, "
               f"{time.time() - t0:.1f}s", flush=True)
     return LIB
+
+
+FASTPATH_SRC = CSRC / "fastpath.c"
+
+
+def fastpath_path() -> Path:
+    import sysconfig
+    return PKG / ("_fastpath" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_fastpath(force: bool = False) -> Path:
+    """The CPython extension for the numpy call path (csrc/fastpath.c),
+    linked against libadaptgemm_b200.so through rpath $ORIGIN/_lib."""
+    import sysconfig
+    out = fastpath_path()
+    deps = [FASTPATH_SRC, INCLUDE / "adaptgemm_b200.h", LIB]
+    if not force and out.exists() and out.stat().st_mtime > max(d.stat().st_mtime for d in deps):
+        return out
+    cmd = ["gcc", "-O2", "-fPIC", "-shared", "-Wall", f"-I{sysconfig.get_paths()['include']}", f"-I{INCLUDE}",
+           str(FASTPATH_SRC), "-o", str(out), f"-L{LIBDIR}", "-ladaptgemm_b200", "-Wl,-rpath,$ORIGIN/_lib"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"fastpath build failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    return out
 
 
 def main(argv=None):

@@ -536,6 +536,23 @@ def _launch_here(shape, config, caps, ops, timed):
     return e0.elapsed_time(e1) * 1e-3
 
 
+_fp = None
+
+
+def _fastpath():
+    """The CPython extension for numpy operands (csrc/fastpath.c), or None
+    when it is not built (the ctypes path below then serves every call)."""
+    global _fp
+    if _fp is None:
+        try:
+            from . import _fastpath as m
+            m.set_errors(ConfigError, ShapeError)
+            _fp = m
+        except ImportError:
+            _fp = False
+    return _fp or None
+
+
 def gemm_execute(shape: ProblemShape, config: KernelConfig, A, B, C,
                  caps: DeviceCaps = DeviceCaps(), out=None):
     """Run one config's family path end to end on the GPU (kernels.py:328-349).
@@ -543,7 +560,20 @@ def gemm_execute(shape: ProblemShape, config: KernelConfig, A, B, C,
     Legality is checked before the operands (ConfigError, then ShapeError).
     Returns (result, seconds); seconds is the CUDA-event device time of the
     whole family path (indirect: pack helpers + tiled core), floored at 1e-9.
+
+    numpy operands (the reference's convention) take the compiled fast path
+    once CUDA is known to be up: one C call does legality, the operand
+    checks and ag_gemm_host_ex (pipelined H2D / family path / D2H with the
+    host buffers page-locked for the call); `seconds` is then the device
+    time of the family path's kernels.
     """
+    if _device._cuda_ok and type(A) is np.ndarray and type(B) is np.ndarray and type(C) is np.ndarray and \
+            (out is None or type(out) is np.ndarray):
+        fp = _fastpath()
+        if fp is not None:
+            r = fp.execute(shape, config, A, B, C, caps, out)
+            if r is not NotImplemented:
+                return r
     if not is_legal(config, caps):
         raise ConfigError(f"illegal config {config.canonical()} for caps {caps}")
     _check_operands(shape, A, B, C)

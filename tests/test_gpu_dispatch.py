@@ -1,5 +1,6 @@
 """Dispatch (compiled selector + GPU launch) and the full CLI pipeline on the GPU."""
 
+import ctypes
 import json
 
 import numpy as np
@@ -267,3 +268,79 @@ def test_acceptance_c11_pipeline_on_gpu(tmp_path, capsys):
         print(f"\n[acceptance C11 on B200] {elapsed:.1f} s (CPU reference 862 s); stages {stage_s}; "
               f"best={best_name} train-dtpr={model_dtpr:.4f} baseline-dtpr={base_dtpr:.4f}")
     assert elapsed < 1800.0
+
+
+def test_numpy_fast_path_matches_and_orders_errors():
+    """The compiled numpy path (csrc/fastpath.c -> ag_gemm_host_ex): same
+    result as the device path, the reference's error order, out in place."""
+    import torch
+
+    from paper_1806_07060_b200.kernels import ConfigError, ShapeError, _fastpath
+    assert _fastpath() is not None, "the _fastpath extension is not built"
+    s = ProblemShape(300, 200, 150, alpha=1.5, beta=0.5)
+    A, B, C = rand_operands(s, seed=61)
+    cfg = KernelConfig.from_canonical("indirect:64-64-16-8-8-2")
+    gemm_execute(s, cfg, A, B, C)  # first call: CUDA verified, fast path enabled
+    out = np.empty((s.M, s.N), np.float32)
+    got, sec = gemm_execute(s, cfg, A, B, C, DeviceCaps(), out)
+    assert got is out and sec > 0
+    dev, _ = gemm_execute(s, cfg, *(torch.from_numpy(x).cuda() for x in (A, B, C)))
+    np.testing.assert_array_equal(out, dev.cpu().numpy())
+    bad = np.ones((3, 3), np.float32)
+    with pytest.raises(ConfigError):
+        gemm_execute(s, KernelConfig(KernelFamily.DIRECT, 8, 8, 8, 1, 1, 2), bad, B, C)
+    with pytest.raises(ShapeError, match="A has shape"):
+        gemm_execute(s, cfg, bad, B, C)
+    with pytest.raises(ShapeError, match="mixed dtypes"):
+        gemm_execute(s, cfg, A, B, C.astype(np.float64))
+
+
+def test_dispatch_and_run_numpy_overhead(capsys):
+    """dispatch_and_run (codegen.py:285-325) with a DecisionTree and numpy
+    operands: the compiled selector is built once per tree, the call is
+    bit-identical to gemm_execute of the selected config, and the Python-side
+    cost of the call (wall time minus the native host-path call) is small."""
+    import time
+
+    from paper_1806_07060_b200 import _native
+    from paper_1806_07060_b200.kernels import native_shape
+    s = ProblemShape(64, 64, 64)
+    A, B, C = rand_operands(s, seed=62)
+    tree = M.train([((64, 64, 64), 0), ((2048, 2048, 2048), 1)])
+    classes = {0: KernelConfig(KernelFamily.DIRECT, 16, 16, 16, 1, 1, 1),
+               1: KernelConfig(KernelFamily.INDIRECT, 64, 64, 16, 8, 8, 2)}
+    r = codegen.dispatch_and_run(tree, s, A, B, C, DeviceCaps(), classes=classes)
+    sel = tree.__dict__["_ag_selectors"][id(classes)][1]
+    r2 = codegen.dispatch_and_run(tree, s, A, B, C, DeviceCaps(), classes=classes)
+    assert tree.__dict__["_ag_selectors"][id(classes)][1] is sel  # cached
+    ref, _ = gemm_execute(s, r.selected, A, B, C)
+    np.testing.assert_array_equal(r.output, ref)
+    np.testing.assert_array_equal(r2.output, ref)
+    # Python-side overhead: the whole call vs the bare native host-path call
+    lib = _native.lib()
+    ns, nc, ncaps = native_shape(s), r.selected.native(), DeviceCaps().native()
+    out = np.empty((64, 64), np.float32)
+    secs = ctypes.c_double()
+
+    def native():
+        lib.ag_gemm_host_ex(ctypes.byref(ns), ctypes.byref(nc), ctypes.byref(ncaps), 0, A.ctypes.data, 64,
+                            B.ctypes.data, 64, C.ctypes.data, 64, out.ctypes.data, 64, None, 0, 0, 1, None,
+                            ctypes.byref(secs))
+
+    def best(fn, n=200):
+        ts = []
+        for _ in range(n):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        ts.sort()
+        return ts[n // 2]
+
+    t_native = best(native)
+    t_exec = best(lambda: gemm_execute(s, r.selected, A, B, C))
+    t_disp = best(lambda: codegen.dispatch_and_run(tree, s, A, B, C, DeviceCaps(), classes=classes))
+    with capsys.disabled():
+        print(f"\n[numpy path 64^3] native host call {t_native * 1e6:.1f} us, gemm_execute "
+              f"{t_exec * 1e6:.1f} us (+{(t_exec - t_native) * 1e6:.1f}), dispatch_and_run {t_disp * 1e6:.1f} us "
+              f"(+{(t_disp - t_native) * 1e6:.1f})")
+    assert t_exec - t_native < 20e-6
