@@ -67,6 +67,17 @@ def geomean(xs):
     return math.exp(sum(math.log(x) for x in xs) / len(xs))
 
 
+def trimmed_mean(xs):
+    """Mean after dropping the lowest and highest quarter.  One GEMM per
+    sample, and B200 CUDA-event timestamps tick in 2.048 us steps
+    (profiles/r02_skinny_probe_*.jsonl), so a median of a microsecond-scale
+    GEMM is stuck on a tick; the mean of the middle samples is not."""
+    xs = sorted(xs)
+    d = len(xs) // 4 if len(xs) >= 4 else 0
+    mid = xs[d:len(xs) - d]
+    return sum(mid) / len(mid)
+
+
 # ---------------------------------------------------------------------------
 # model: the reference pipeline on the shipped B200 tables
 
@@ -516,7 +527,7 @@ def run_ours(args):
     clocks = clocks_summary(proc, clk_path)
     region_s = r0.elapsed_time(r1) * 1e-3
     per_step = [times(evs) for evs in step_evs]
-    dt_t = [statistics.median(p[i] for p in per_step) for i in range(len(cases))]
+    dt_t = [trimmed_mean([p[i] for p in per_step]) for i in range(len(cases))]
     dt_t = distributed.reduce_max(dt_t, device)
     region_s = distributed.reduce_max([region_s], device)[0]
 
@@ -525,10 +536,10 @@ def run_ours(args):
     default_cfgs = [policy.select_config(c.shape) for c in cases]
     dt_cfgs = [selector.select(*c.shape.mnk) for c in cases]
 
-    def measured(cs, cfgs):
-        runs = [times(fixed_pass(cs, cfgs)) for _ in range(max(3, args.steps // 2))]
+    def measured(cs, cfgs, reps=None):
+        runs = [times(fixed_pass(cs, cfgs)) for _ in range(reps or max(4, args.steps))]
         torch.cuda.synchronize()
-        return distributed.reduce_max([statistics.median(r[i] for r in runs) for i in range(len(cs))], device)
+        return distributed.reduce_max([trimmed_mean([r[i] for r in runs]) for i in range(len(cs))], device)
 
     fixed_pass(cases, oracle_cfgs)
     oracle_t = measured(cases, oracle_cfgs)
@@ -549,14 +560,38 @@ def run_ours(args):
     rate = lambda cs, ts: [c.flops / t / 1e9 for c, t in zip(cs, ts)]  # noqa: E731
     dt_r, or_r, de_r = rate(cases, dt_t), rate(cases, oracle_t), rate(cases, default_t)
     value_1 = geomean(dt_r)
+    unseen_set = {s.mnk for s in m["db_unseen"]}
+    unseen = [i for i, c in enumerate(cases) if c.shape.mnk in unseen_set]
 
     # po2 held-out split (configs[1])
-    po2_steps = max(3, args.steps // 3)
+    po2_steps = max(4, args.steps // 3)
     po2_runs = [times(dt_pass(po2_cases)) for _ in range(po2_steps)]
     torch.cuda.synchronize()
-    po2_dt = [statistics.median(r[i] for r in po2_runs) for i in range(len(po2_cases))]
-    po2_or = measured(po2_cases, [tables[c.shape.mnk].best_config for c in po2_cases])
-    po2_de = measured(po2_cases, [policy.select_config(c.shape) for c in po2_cases])
+    po2_dt = [trimmed_mean([r[i] for r in po2_runs]) for i in range(len(po2_cases))]
+    po2_or = measured(po2_cases, [tables[c.shape.mnk].best_config for c in po2_cases], po2_steps)
+    po2_de = measured(po2_cases, [policy.select_config(c.shape) for c in po2_cases], po2_steps)
+    # configs[1] is po2 64..4096: its held-out shapes are the test-split shapes with every dim >= 64
+    in_c1 = [i for i, c in enumerate(po2_cases) if min(c.shape.mnk) >= 64]
+
+    # ---- secondary model: the reference CLI's hybrid dataset (po2 + DeepBench,
+    # one 80/20 split), DT on DeepBench reported per subset (cli.py:413-420)
+    hy = build_hybrid_model()
+    hy_sel = codegen.CompiledSelector(hy["tree"], hy["classes"])
+    hy_runs = [times(runner.pass_(cases, lambda i, c: runner.launch(c, selector=hy_sel, fallback=fallback)))
+               for _ in range(max(4, args.steps // 2))]
+    torch.cuda.synchronize()
+    hy_t = distributed.reduce_max([trimmed_mean([r[i] for r in hy_runs]) for i in range(len(cases))], device)
+    case_idx = {c.shape.mnk: i for i, c in enumerate(cases)}
+
+    def hy_sub(shapes):
+        idx = [case_idx[s.mnk] for s in shapes]
+        if not idx:
+            return {"shapes": 0}
+        d = geomean(cases[i].flops / hy_t[i] / 1e9 for i in idx)
+        o = geomean(cases[i].flops / oracle_t[i] / 1e9 for i in idx)
+        q = geomean(cases[i].flops / default_t[i] / 1e9 for i in idx)
+        return {"shapes": len(idx), "dt_geomean": round(d, 2), "oracle_geomean": round(o, 2),
+                "default_geomean": round(q, 2), "dt_over_oracle": round(d / o, 4), "dt_over_default": round(d / q, 4)}
 
     # ---- configs[4]: the tensor-core search space on random (M, N, K)
     # sub-measurements never take the headline line down with them
@@ -569,29 +604,42 @@ def run_ours(args):
     except Exception as exc:  # noqa: BLE001
         go2_doc = {"error": f"{type(exc).__name__}: {exc}"}
     # ---- configs[3]: sharded exhaustive sweep throughput
-    sweep_doc = sweep_section(device, distributed, rank, world) if not args.no_sweep else None
+    sweep_doc = sweep_section(device, distributed, rank, world,
+                              with_cpu=(rank == 0 and world == 1 and not args.no_cpu_baseline)) \
+        if not args.no_sweep else None
 
-    # ---- e2e: the public API with host buffers, copies inside the timed call
+    # ---- e2e: the reference-facing call with the reference's own data
+    # convention -- codegen.dispatch_and_run(tree, shape, A, B, C, caps) on
+    # plain (pageable) numpy arrays (codegen.py:285-325) -- copies inside.
     from paper_1806_07060_b200.kernels import reads_c
-    e2e_t = []
+    e2e_t, pinned_t = [], []
     h2d = d2h = 0
     for c, cfg in zip(cases, dt_cfgs):
-        # inputs live in pinned host memory (allocated outside the timed call)
-        A, B, C = (torch.from_numpy(x).pin_memory() for x in c.host)
-        hout = torch.empty((c.shape.M, c.shape.N), dtype=torch.float32).pin_memory()
-        best = None
+        A, B, C = c.host
+        codegen.dispatch_and_run(tree, c.shape, A, B, C, caps, classes=classes)  # warm (selector, page-lock path)
+        ts = []
         for _ in range(3):
-            torch.cuda.synchronize()
             t0 = time.perf_counter()
-            out, picked, _fb = codegen.dispatch_native(selector, c.shape, A, B, C, caps, out=hout)
-            t1 = time.perf_counter()
-            best = (t1 - t0) if best is None else min(best, t1 - t0)
-        e2e_t.append(best)
-        # bytes the API moved: C only when the chosen family reads it
-        h2d += A.numel() * 4 + B.numel() * 4 + (C.numel() * 4 if reads_c(c.shape, picked) else 0)
-        d2h += hout.numel() * 4
+            res = codegen.dispatch_and_run(tree, c.shape, A, B, C, caps, classes=classes)
+            ts.append(time.perf_counter() - t0)
+        e2e_t.append(statistics.median(ts))
+        picked = res.selected
+        h2d += A.nbytes + B.nbytes + (C.nbytes if reads_c(c.shape, picked) else 0)
+        d2h += res.output.nbytes
+        # the same call from pinned torch buffers (dispatch_native), for comparison
+        pA, pB, pC = (torch.from_numpy(x).pin_memory() for x in c.host)
+        hout = torch.empty((c.shape.M, c.shape.N), dtype=torch.float32).pin_memory()
+        codegen.dispatch_native(selector, c.shape, pA, pB, pC, caps, out=hout)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            codegen.dispatch_native(selector, c.shape, pA, pB, pC, caps, out=hout)
+            ts.append(time.perf_counter() - t0)
+        pinned_t.append(statistics.median(ts))
     e2e_t = distributed.reduce_max(e2e_t, device)
+    pinned_t = distributed.reduce_max(pinned_t, device)
     e2e_value = geomean(rate(cases, e2e_t))
+    e2e_pinned = geomean(rate(cases, pinned_t))
     # spot-check the DT output against the float64 product (first rows)
     c0 = max(cases, key=lambda c: c.flops)
     rows = slice(0, 8)
@@ -630,9 +678,11 @@ def run_ours(args):
         "data": "synthetic (reference _bench_buffers recipe: PCG64(mix(0,M,N,K)) U(-1,1))",
         "config": {"workload": "deepbench_fp32: DeepBench-style rectangular set (BASELINE configs[2])",
                    "shapes": len(cases), "alpha": 1.0, "beta": 0.0, "trans": "NN",
-                   "l2": "flushed (256 MB write) before every timed GEMM",
+                   "l2": "flushed (256 MB write) before every timed GEMM; per-shape time = trimmed mean "
+                         "(middle half) of the steps' event times",
                    "parallelism": f"replicas x{world} (shapes independent; no collective on the data path)",
-                   "model": f"{m['name']} trained on {m['n_train']} shapes (po2 + DeepBench train splits)",
+                   "model": f"{m['name']} trained on {m['n_train']} po2 shapes ({m['train_set']}); no DeepBench "
+                            "shape in training or model selection",
                    "caps_profile": "b200"},
         "dt_vs": {"dt_geomean": round(value_1, 2), "oracle_geomean": round(geomean(or_r), 2),
                   "default_geomean": round(geomean(de_r), 2),
@@ -641,11 +691,23 @@ def run_ours(args):
                   "default_config": [policy.default_direct.canonical(), policy.default_indirect.canonical()],
                   "default_sensitivity": [dict(s, dt_over_default=round(value_1 / s["default_geomean"], 4))
                                           for s in sensitivity],
-                  "held_out_shapes": [list(s.mnk) for s in m["db_test"]]},
-        "po2_test_split": {"shapes": len(po2_cases),
+                  "unseen": {"shapes": len(unseen), "note": "DeepBench shapes that are not po2 training shapes",
+                             "dt_geomean": round(geomean(dt_r[i] for i in unseen), 2),
+                             "oracle_geomean": round(geomean(or_r[i] for i in unseen), 2),
+                             "default_geomean": round(geomean(de_r[i] for i in unseen), 2)}},
+        "hybrid_model": {"model": hy["name"], "n_train": hy["n_train"], "n_test": hy["n_test"],
+                         "note": "reference CLI hybrid dataset (po2 + DeepBench, one 80/20 split); DT measured "
+                                 "live on the DeepBench shapes of each subset",
+                         "deepbench_train": hy_sub(hy["db_train"]), "deepbench_test": hy_sub(hy["db_test"])},
+        "po2_test_split": {"shapes": len(po2_cases), "dataset": "po2 16..4096 (held-out 20 %)",
                            "dt_geomean": round(geomean(rate(po2_cases, po2_dt)), 2),
                            "oracle_geomean": round(geomean(rate(po2_cases, po2_or)), 2),
-                           "default_geomean": round(geomean(rate(po2_cases, po2_de)), 2)},
+                           "default_geomean": round(geomean(rate(po2_cases, po2_de)), 2),
+                           "configs1_po2_64_4096": {
+                               "shapes": len(in_c1),
+                               "dt_geomean": round(geomean(rate(po2_cases, po2_dt)[i] for i in in_c1), 2),
+                               "oracle_geomean": round(geomean(rate(po2_cases, po2_or)[i] for i in in_c1), 2),
+                               "default_geomean": round(geomean(rate(po2_cases, po2_de)[i] for i in in_c1), 2)}},
         "model_scores_table_mode": m["score"],
         "per_shape": [[list(c.shape.mnk), round(d, 1), round(o, 1), round(q, 1), dc.canonical(),
                        oc.canonical(), qc.canonical()]
@@ -654,9 +716,12 @@ def run_ours(args):
                               "oracle_config", "default_config"],
         "e2e": {"value": round(e2e_value * world, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "how": "codegen.dispatch_native(selector, shape, pinned torch CPU A, B, C, out=pinned) -> "
-                       "ag_dispatch_gemm_host: H2D, family path and D2H pipelined over output panels on three "
-                       "streams, one blocking call; best of 3 wall-clock calls per shape"},
+                "how": "codegen.dispatch_and_run(tree, shape, A, B, C, caps, classes) on plain pageable numpy "
+                       "arrays (the reference's call, codegen.py:285-325): cached compiled selector, then the "
+                       "compiled numpy path (csrc/fastpath.c) -> ag_gemm_host_ex: host buffers page-locked for "
+                       "the call, H2D / family path / D2H pipelined over output panels on three streams; median "
+                       "of 3 wall-clock calls per shape",
+                "pinned_dispatch_native": round(e2e_pinned * world, 2)},
         "roofline": {"bound": "fp32-cuda-core (compute)", "achieved": round(achieved, 3),
                      "peak": round(peak_meas, 3), "unit": "TFLOP/s", "frac": round(achieved / peak_meas, 4),
                      "traffic": traffic, "kernel": key,
@@ -746,40 +811,106 @@ def tc_section(m, policy, device, distributed, times, fallback, args):
                           for c, a, b, d, o in zip(cases, rate(dt_t), rate(or_t), dt_cfgs, or_cfgs)]}
 
 
-def sweep_section(device, distributed, rank, world):
-    """configs[3]: the exhaustive tuning sweep (B200 profile, timing 1 + 3,
-    the sweep the shipped tables came from) over a fixed 16-shape set
-    (M = N and K in {128, 256, 512, 1024}), LPT-sharded shape-wise over the
+def _cpu_sweep_worker(job):
+    """One single-threaded reference-CPU process of `tune --jobs nproc`
+    (cli.py:198-228): times its shapes' sampled configs with the oracle port
+    of the reference's numba kernels, warmup + repeats runs each."""
+    shapes, cfgs, warmup, repeats = job
+    from oracle import gemm as ogemm
+    from paper_1806_07060_b200.kernels import KernelConfig
+    from paper_1806_07060_b200.tuner import _bench_buffers
+    ogemm.set_threads(1)
+    n = 0
+    flops = 0.0
+    for mnk in shapes:
+        from paper_1806_07060_b200.kernels import ProblemShape
+        sh = ProblemShape(*mnk)
+        A, B, C, _ = _bench_buffers(sh, np.float32, 0)
+        for canon in cfgs:
+            c = KernelConfig.from_canonical(canon)
+            for _ in range(warmup + repeats):
+                ogemm.execute(sh.M, sh.N, sh.K, 1.0, 0.0, False, False, A, B, C, c.family.value, *c.param_tuple())
+            n += 1
+            flops += 2.0 * sh.M * sh.N * sh.K * (warmup + repeats)
+    return n, flops
+
+
+def cpu_sweep(shapes, stride=8, warmup=1, repeats=3):
+    """The reference's CPU sweep of the same shapes on all host cores (one
+    single-threaded process per core, as `tune --jobs $(nproc)`), on every
+    `stride`-th config of the reference space: configs/s measured, the full
+    sweep's wall time extrapolated (labelled an estimate)."""
+    import concurrent.futures
+    import multiprocessing
+
+    from oracle import gemm as ogemm
+    from paper_1806_07060_b200.kernels import DeviceCaps, full_search_space
+    from paper_1806_07060_b200.sharding import lpt_partition
+    ogemm.build()
+    space = [c.canonical() for c in full_search_space(DeviceCaps())]
+    sample = space[::stride]
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    parts = [p for p in lpt_partition([s.mnk for s in shapes], cores, lambda m: m[0] * m[1] * m[2]) if p]
+    t0 = time.perf_counter()
+    with concurrent.futures.ProcessPoolExecutor(max_workers=len(parts),
+                                                mp_context=multiprocessing.get_context("spawn")) as ex:
+        res = list(ex.map(_cpu_sweep_worker, [(p, sample, warmup, repeats) for p in parts]))
+    wall = time.perf_counter() - t0
+    n = sum(r[0] for r in res)
+    flops = sum(r[1] for r in res)
+    full = len(space) * len(shapes)
+    return {"configs_timed": n, "configs_per_shape_sampled": len(sample), "configs_per_shape_full": len(space),
+            "wall_s": round(wall, 2), "configs_per_s": round(n / wall, 2),
+            "swept_gflops_per_s": round(flops / wall / 1e9, 2), "processes": len(parts), "cores": cores,
+            "full_sweep_wall_s_estimate": round(full / (n / wall), 1),
+            "shapes_per_h_estimate": round(len(shapes) / (full / (n / wall)) * 3600, 1),
+            "kind": "port", "how": f"oracle port of the reference's numba kernels, one single-threaded process "
+                                   f"per core (tune --jobs nproc), every {stride}th config of the 576-config "
+                                   f"reference space, warmup {warmup} + repeats {repeats}"}
+
+
+def sweep_section(device, distributed, rank, world, with_cpu):
+    """configs[3]: the exhaustive tuning sweep of acceptance C11's dataset,
+    po2(64, 256) = 27 shapes, timing warmup 1 + repeats 3 (the reference's
+    smoke config, test_acceptance.py:339-387), LPT-sharded shape-wise over the
     ranks with no collective (cli tune --gpus); wall time = max over ranks.
-    Total work is fixed, so this sub-measurement scales strongly."""
+    Both the reference space (576 configs, what the CPU sweep times) and the
+    B200 profile; the reference's CPU sweep of the same shapes beside it."""
     import torch
 
     from paper_1806_07060_b200 import distributed as dist_mod
+    from paper_1806_07060_b200.dataset import gen_po2
     from paper_1806_07060_b200.kernels import DeviceCaps, ProblemShape, full_search_space
     from paper_1806_07060_b200.sharding import sweep_cost
     from paper_1806_07060_b200.tuner import TimingPolicy, tune_exhaustive
 
-    caps = DeviceCaps.b200()
     timing = TimingPolicy(warmup=1, repeats=3)
-    dims = (128, 256, 512, 1024)
-    shapes = [ProblemShape(mn, mn, k) for mn in dims for k in dims]
-    n_cfg = len(full_search_space(caps))
-    mine = dist_mod.shard(shapes, rank, world, lambda s: sweep_cost(s.mnk, n_cfg, 8))
-    tune_exhaustive(ProblemShape(64, 64, 64), caps, timing)  # warm every kernel once
-    distributed.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for s in mine:
-        tune_exhaustive(s, caps, timing)
-    torch.cuda.synchronize()
-    wall = distributed.reduce_max([time.perf_counter() - t0], device)[0]
-    flops = sum(2.0 * s.M * s.N * s.K for s in shapes)
-    return {"shapes": len(shapes), "configs_per_shape": n_cfg, "configs_timed": n_cfg * len(shapes),
-            "wall_s": round(wall, 3), "configs_per_s": round(n_cfg * len(shapes) / wall, 1),
-            "shapes_per_s": round(len(shapes) / wall, 3), "ranks": world, "scaling": "strong",
-            "swept_tflop": round(flops * n_cfg / 1e12, 3),
-            "how": "tune_exhaustive per shape on this rank's LPT shard; wall clock around the shard, "
-                   "max over ranks (device-timed samples inside, CUDA events)"}
+    shapes = [s if isinstance(s, ProblemShape) else ProblemShape(*s) for s in gen_po2(64, 256)]
+    out = {"shapes": len(shapes), "dataset": "po2(64, 256) (acceptance C11)", "ranks": world, "scaling": "strong",
+           "timing": "warmup 1 + repeats 3 (warm)"}
+    tune_exhaustive(ProblemShape(64, 64, 64), DeviceCaps.b200(), timing)  # warm every kernel once
+    for name, caps in (("reference_space", DeviceCaps()), ("b200_space", DeviceCaps.b200())):
+        n_cfg = len(full_search_space(caps))
+        mine = dist_mod.shard(shapes, rank, world, lambda s: sweep_cost(s.mnk, n_cfg, 8))
+        distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in mine:
+            tune_exhaustive(s, caps, timing)
+        torch.cuda.synchronize()
+        wall = distributed.reduce_max([time.perf_counter() - t0], device)[0]
+        flops = sum(2.0 * s.M * s.N * s.K for s in shapes) * n_cfg * (timing.warmup + timing.repeats)
+        out[name] = {"configs_per_shape": n_cfg, "configs_timed": n_cfg * len(shapes), "wall_s": round(wall, 3),
+                     "configs_per_s": round(n_cfg * len(shapes) / wall, 1),
+                     "shapes_per_h": round(len(shapes) / wall * 3600, 1),
+                     "swept_gflops_per_s": round(flops / wall / 1e9, 1)}
+    if with_cpu:
+        cpu = cpu_sweep(shapes)
+        out["cpu_reference"] = cpu
+        out["gpu_over_cpu_configs_per_s"] = round(out["reference_space"]["configs_per_s"] / cpu["configs_per_s"], 1)
+    out["how"] = ("tune_exhaustive per shape on this rank's LPT shard; wall clock around the shard, max over "
+                  "ranks (device-timed samples inside, CUDA events)")
+    return out
 
 
 def main(argv=None):

@@ -368,6 +368,21 @@ struct HostPipe {
     std::vector<cudaEvent_t> tev;  // timing events around each panel's family path
     void* scratch = nullptr;       // ag_device_scratch: grow-only, per thread and device
     size_t scratch_bytes = 0;
+    void* pinned = nullptr;        // small-call staging (cudaHostAlloc), grow-only
+    size_t pinned_bytes = 0;
+    void* pinned_buffer(size_t bytes) {
+        if (pinned && pinned_bytes >= bytes) return pinned;
+        if (pinned) cudaFreeHost(pinned);
+        pinned = nullptr;
+        pinned_bytes = 0;
+        if (cudaHostAlloc(&pinned, bytes, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            pinned = nullptr;
+            return nullptr;
+        }
+        pinned_bytes = bytes;
+        return pinned;
+    }
     cudaEvent_t timing_event(size_t i) {
         while (tev.size() <= i) {
             cudaEvent_t e;
@@ -619,6 +634,72 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
     if (dev_bytes < h.total) return set_err(AG_ERR_SHAPE, "device scratch too small for the host path");
     HostPipe& t_pipe = pipe();
     if (!t_pipe.ok()) return set_err(AG_ERR_CUDA, "cannot create the host-path streams");
+    // Small calls (<= 4 MB moved, one panel): pack the operands into one
+    // pinned staging block with the CPU, ONE H2D DMA, the family path, ONE
+    // D2H DMA, one stream synchronize -- instead of a pageable copy (the
+    // driver's synchronous staging) per operand and three streams.
+    {
+        const int64_t e = h.elem, M = s->m, N = s->n;
+        const size_t a_b = (size_t)(h.ra * h.ca * e), b_b = (size_t)(h.rb * h.cb * e);
+        const size_t c_b = h.reads_c ? (size_t)(M * N * e) : 0, o_b = (size_t)(M * N * e);
+        const size_t in_b = a_b + b_b + c_b;
+        char* stage = (h.panels == 1 && in_b + o_b <= (4u << 20)) ? (char*)t_pipe.pinned_buffer(4u << 20) : nullptr;
+        if (stage) {
+            auto pack = [&](char* dst, const void* src, int64_t rows, int64_t cols, int64_t ld) {
+                const char* sp = static_cast<const char*>(src);
+                if (ld == cols) {
+                    memcpy(dst, sp, (size_t)(rows * cols * e));
+                } else {
+                    for (int64_t r = 0; r < rows; ++r) memcpy(dst + r * cols * e, sp + r * ld * e, (size_t)(cols * e));
+                }
+            };
+            pack(stage, A, h.ra, h.ca, lda);
+            pack(stage + a_b, B, h.rb, h.cb, ldb);
+            if (c_b) pack(stage + a_b + b_b, C, M, N, ldc);
+            char* base = static_cast<char*>(dev);
+            char *dA = base + h.offA, *dB = base + h.offB, *dC = base + h.offC, *dO = base + h.offO;
+            cudaStream_t run = t_pipe.s[1];
+            cudaError_t ce = cudaSuccess;
+            auto ok = [&](cudaError_t x) { if (x != cudaSuccess && ce == cudaSuccess) ce = x; };
+            cudaEvent_t start = t_pipe.event(0);
+            if (!start) return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
+            ok(cudaEventRecord(start, static_cast<cudaStream_t>(stream)));
+            ok(cudaStreamWaitEvent(run, start, 0));
+            // the staging block mirrors [A | B | C] in device scratch when they are adjacent there
+            if (dB == dA + a_b && (!c_b || dC == dB + b_b)) {
+                ok(cudaMemcpyAsync(dA, stage, in_b, cudaMemcpyHostToDevice, run));
+            } else {
+                ok(cudaMemcpyAsync(dA, stage, a_b, cudaMemcpyHostToDevice, run));
+                ok(cudaMemcpyAsync(dB, stage + a_b, b_b, cudaMemcpyHostToDevice, run));
+                if (c_b) ok(cudaMemcpyAsync(dC, stage + a_b + b_b, c_b, cudaMemcpyHostToDevice, run));
+            }
+            cudaEvent_t k0 = kernel_seconds ? t_pipe.timing_event(0) : nullptr;
+            cudaEvent_t k1 = kernel_seconds ? t_pipe.timing_event(1) : nullptr;
+            if (k0) ok(cudaEventRecord(k0, run));
+            void* dW = h.wsz ? base + h.offW : nullptr;
+            r = fn(make_call(s, c, dtype, dA, h.ca, dB, h.cb, c_b ? (const void*)dC : (const void*)dO, N, dO, N, dW,
+                             h.wsz, run));
+            if (r) {
+                cudaStreamSynchronize(run);
+                return r;
+            }
+            if (k1) ok(cudaEventRecord(k1, run));
+            char* ostage = stage + ((in_b + 255) / 256) * 256;
+            if (ostage + o_b > stage + (4u << 20)) ostage = stage;  // inputs are consumed before the D2H lands
+            ok(cudaMemcpyAsync(ostage, dO, o_b, cudaMemcpyDeviceToHost, run));
+            ok(cudaStreamSynchronize(run));
+            if (ce != cudaSuccess) return set_err(AG_ERR_CUDA, std::string("host path: ") + cudaGetErrorString(ce));
+            char* op = static_cast<char*>(out);
+            for (int64_t rr = 0; rr < M; ++rr) memcpy(op + rr * ldo * e, ostage + rr * N * e, (size_t)(N * e));
+            if (kernel_seconds) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, k0, k1);
+                *kernel_seconds = std::max(ms * 1e-3, 1e-9);
+            }
+            cudaError_t le = cudaGetLastError();
+            return le == cudaSuccess ? AG_OK : set_err(AG_ERR_CUDA, cudaGetErrorString(le));
+        }
+    }
     HostLocks locks;
     if (flags & AG_HOST_REGISTER) {
         locks.lock(A, h.ra, lda, h.ca, h.elem);

@@ -64,7 +64,7 @@ def test_binding_large_pageable_call(binding):
     from paper_1806_07060_b200.tuner import _bench_buffers
     s = ProblemShape(2048, 3000, 1024)
     A, B, C, _ = _bench_buffers(s, np.float32, 0)
-    out, sec = binding.gemm_execute(s, KernelConfig.from_canonical("indirect:64-64-16-8-8-2"), A, B, C,
+    out, sec = binding.gemm_execute(s, KernelConfig.from_canonical("indirect:64-64-16-8-4-2"), A, B, C,
                                     DeviceCaps())
     exact = A.astype(np.float64) @ B.astype(np.float64)
     assert rel_frobenius(out, exact) <= 1e-5 and sec > 0

@@ -279,7 +279,7 @@ def test_numpy_fast_path_matches_and_orders_errors():
     assert _fastpath() is not None, "the _fastpath extension is not built"
     s = ProblemShape(300, 200, 150, alpha=1.5, beta=0.5)
     A, B, C = rand_operands(s, seed=61)
-    cfg = KernelConfig.from_canonical("indirect:64-64-16-8-8-2")
+    cfg = KernelConfig.from_canonical("indirect:64-64-16-8-4-2")
     gemm_execute(s, cfg, A, B, C)  # first call: CUDA verified, fast path enabled
     out = np.empty((s.M, s.N), np.float32)
     got, sec = gemm_execute(s, cfg, A, B, C, DeviceCaps(), out)
@@ -308,7 +308,7 @@ def test_dispatch_and_run_numpy_overhead(capsys):
     A, B, C = rand_operands(s, seed=62)
     tree = M.train([((64, 64, 64), 0), ((2048, 2048, 2048), 1)])
     classes = {0: KernelConfig(KernelFamily.DIRECT, 16, 16, 16, 1, 1, 1),
-               1: KernelConfig(KernelFamily.INDIRECT, 64, 64, 16, 8, 8, 2)}
+               1: KernelConfig(KernelFamily.INDIRECT, 64, 64, 16, 8, 4, 2)}
     r = codegen.dispatch_and_run(tree, s, A, B, C, DeviceCaps(), classes=classes)
     sel = tree.__dict__["_ag_selectors"][id(classes)][1]
     r2 = codegen.dispatch_and_run(tree, s, A, B, C, DeviceCaps(), classes=classes)

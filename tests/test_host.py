@@ -610,3 +610,40 @@ def test_merge_tables_keeps_base_and_order():
     assert m.find(c2).gflops == 2.0 and m.best_config == c3
     with pytest.raises(ValueError):
         merge_tables(a, TuningTable.from_measurements(s, [Measurement(c3, 1.0, 1.0)], dict(meta, repeats="5")))
+
+
+def test_shipped_b200_models_match_reference():
+    """The models bench.py trains on the shipped B200 tables equal the
+    reference's own CART on the same records: split indices, all 40 grid
+    fingerprints and every model's predictions on the DeepBench shapes
+    (tests/golden/make_b200_golden.py ran the reference itself)."""
+    import json
+
+    import bench
+    from paper_1806_07060_b200 import codegen, model
+    from paper_1806_07060_b200.dataset import dataset_from_tables, split
+    from paper_1806_07060_b200.tuner import load_table_bundle
+    path = GOLDEN / "b200_trees.json"
+    doc = json.loads(path.read_text())
+    po2 = load_table_bundle(bench.PO2_BUNDLE)
+    db = load_table_bundle(bench.DB_BUNDLE)
+    assert doc["bundles"] == [bench.PO2_BUNDLE.name, bench.DB_BUNDLE.name]
+    hybrid, seen = [], set()
+    for t in po2 + db:
+        if t.shape.mnk not in seen:
+            seen.add(t.shape.mnk)
+            hybrid.append(t)
+    probes = [tuple(p) for p in doc["probe_shapes"]]
+    for key, tables, prov in (("po2", po2, "po2"), ("hybrid", hybrid, "hybrid")):
+        want = doc[key]
+        ds = dataset_from_tables(tables, prov)
+        recs = ds.features_and_labels()
+        assert [c for _, c in recs] == want["labels"]
+        sp = split(ds, bench.SPLIT_FRACTION, bench.SPLIT_SEED)
+        assert list(sp.train) == want["train"] and list(sp.test) == want["test"]
+        named = model.grid_train([recs[i] for i in sp.train])
+        assert len(named) == len(want["trees"]) == 40
+        for name, tree in named:
+            w = want["trees"][name]
+            assert codegen.tree_fingerprint(tree) == w["fingerprint"], (key, name)
+            assert [model.predict(tree, p) for p in probes] == w["predictions"], (key, name)
