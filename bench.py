@@ -236,6 +236,20 @@ def go2_section():
             "paper_p100_go2_hmax_l1": {"accuracy": 0.60, "dtpr": 0.852, "dttr": 1.424}}
 
 
+def deepbench_table_mode(m, selector):
+    """The reference's DTPR / DTTR (arithmetic means of per-shape ratios,
+    evaluation.py:169-183) of the headline model on the DeepBench tables:
+    DT pick vs the table's best (DTPR) and vs the default tile (DTTR)."""
+    dtpr, dttr = [], []
+    for s in m["db_all"]:
+        t = m["tables"][s.mnk]
+        g = t.gflops_for(selector.select(*s.mnk))
+        dtpr.append(g / t.peak_gflops)
+        dttr.append(g / t.gflops_for(m["policy"].select_config(s)))
+    return {"shapes": len(dtpr), "dtpr": round(math.fsum(dtpr) / len(dtpr), 4),
+            "dttr": round(math.fsum(dttr) / len(dttr), 4)}
+
+
 def ProblemShapeOf(mnk):
     from paper_1806_07060_b200.kernels import ProblemShape
     return ProblemShape(*mnk)
@@ -709,6 +723,7 @@ def run_ours(args):
                                "oracle_geomean": round(geomean(rate(po2_cases, po2_or)[i] for i in in_c1), 2),
                                "default_geomean": round(geomean(rate(po2_cases, po2_de)[i] for i in in_c1), 2)}},
         "model_scores_table_mode": m["score"],
+        "deepbench_table_mode": deepbench_table_mode(m, selector),
         "per_shape": [[list(c.shape.mnk), round(d, 1), round(o, 1), round(q, 1), dc.canonical(),
                        oc.canonical(), qc.canonical()]
                       for c, d, o, q, dc, oc, qc in zip(cases, dt_r, or_r, de_r, dt_cfgs, oracle_cfgs, default_cfgs)],
