@@ -68,6 +68,13 @@ extern "C" {
  *     K slices. */
 #define AG_FAMILY_SKINNY_N 6
 #define AG_FAMILY_SKINNY_M 7
+/* b200tc profile: fp32-accurate GEMM on the tensor pipe ("3xTF32").  Each
+ * fp32 operand is split as x = hi + lo (hi = the bits a tf32 MMA reads,
+ * lo = x - hi, staged by one convert pass); a.b ~ a_hi.b_hi + a_hi.b_lo +
+ * a_lo.b_hi as three tcgen05 kind::tf32 MMAs per K step into one TMEM
+ * accumulator.  Meets the fp32 families' RF <= 1e-5 contract.  Tile fields
+ * as the tf32 family (bm 128 / 256, bn, bk = 32, tm = stages). */
+#define AG_FAMILY_TF32X3 8
 
 /* element types accepted by gemm_execute (kernels.py:282-283) */
 #define AG_F32 0
@@ -153,6 +160,12 @@ int ag_gemm_host(const ag_shape* shape, const ag_config* config, const ag_caps* 
  * time of the family path (CUDA events around each panel's kernels, summed),
  * the reference's `seconds` without the copies. */
 #define AG_HOST_REGISTER 1
+/* flags & AG_HOST_STAGE: pageable host buffers cross through two
+ * library-owned pinned rings (4 x 16 MB each per thread and device): a pool
+ * of host copy workers fills / drains ring slots while the copy engines move
+ * the neighbouring slots and the kernels run.  Pinned buffers are DMA'd
+ * directly.  Takes precedence over AG_HOST_REGISTER for pageable buffers. */
+#define AG_HOST_STAGE 2
 int ag_gemm_host_ex(const ag_shape* shape, const ag_config* config, const ag_caps* caps, int dtype,
                     const void* A, int64_t lda, const void* B, int64_t ldb,
                     const void* C, int64_t ldc, void* out, int64_t ldo,

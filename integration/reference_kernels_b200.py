@@ -14,8 +14,8 @@ It replaces the body of /root/reference/pkg/src/adaptgemm/kernels.py:328-349
 
 Dependencies are the reference's own: numpy + ctypes.  No torch: the device
 scratch is the library's own (ag_device_scratch), the copies are pipelined
-inside ag_gemm_host_ex and the caller's pageable arrays are page-locked for
-the duration of the call (AG_HOST_REGISTER).
+inside ag_gemm_host_ex and the caller's pageable arrays cross through the
+library's pinned staging rings (AG_HOST_STAGE).
 
     import reference_kernels_b200 as b200
     b200.bind(kernels.ConfigError, kernels.ShapeError)   # the reference's classes
@@ -62,7 +62,7 @@ class _Caps(ctypes.Structure):
 
 # include/adaptgemm_b200.h AG_FAMILY_*; the reference has the first two
 _FAMILY = {"direct": 0, "indirect": 1, "splitk": 2, "tf32": 3, "bf16": 4, "tma": 5, "skinny_n": 6, "skinny_m": 7}
-AG_HOST_REGISTER = 1
+AG_HOST_STAGE = 2
 _P, _I = ctypes.c_void_p, ctypes.c_int64
 _lib = None
 
@@ -125,7 +125,7 @@ def gemm_execute(shape, config, A, B, C, caps, out=None):
     secs = ctypes.c_double(0.0)
     rc = L.ag_gemm_host_ex(ctypes.byref(s), ctypes.byref(c), ctypes.byref(k), 0 if A.dtype == np.float32 else 1,
                            A.ctypes.data, A.shape[1], B.ctypes.data, B.shape[1], C.ctypes.data, C.shape[1],
-                           dst.ctypes.data, dst.shape[1], None, 0, 0, AG_HOST_REGISTER, None, ctypes.byref(secs))
+                           dst.ctypes.data, dst.shape[1], None, 0, 0, AG_HOST_STAGE, None, ctypes.byref(secs))
     if rc:
         msg = (L.ag_last_error() or b"").decode()
         raise (ConfigError if rc == 1 else ShapeError if rc == 2 else RuntimeError)(msg)

@@ -14,10 +14,12 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libadaptgemm_b200.so"
 
 AG_OK, AG_ERR_CONFIG, AG_ERR_SHAPE, AG_ERR_CUDA = 0, 1, 2, 3
 AG_HOST_REGISTER = 1  # ag_gemm_host_ex flag: page-lock the caller's host buffers for the call
+AG_HOST_STAGE = 2  # ag_gemm_host_ex flag: pageable buffers through the library's pinned rings
 AG_FAMILY_DIRECT, AG_FAMILY_INDIRECT, AG_FAMILY_SPLITK = 0, 1, 2
 AG_FAMILY_TF32, AG_FAMILY_BF16 = 3, 4
 AG_FAMILY_TMA = 5
 AG_FAMILY_SKINNY_N, AG_FAMILY_SKINNY_M = 6, 7
+AG_FAMILY_TF32X3 = 8
 AG_F32, AG_F64 = 0, 1
 
 

@@ -41,7 +41,7 @@ CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-O2", "-fPIC", "-std=c++17", "-Wall", f"-I{INCLUDE}"]
 
 N_UNITS = 48
-FAMILY_CODE = {"direct": 0, "indirect": 1, "splitk": 2, "tf32": 3, "bf16": 4, "tma": 5, "skinny_n": 6, "skinny_m": 7}
+FAMILY_CODE = {"direct": 0, "indirect": 1, "splitk": 2, "tf32": 3, "bf16": 4, "tma": 5, "skinny_n": 6, "skinny_m": 7, "tf32x3": 8}
 
 
 def _cost(t):
@@ -87,7 +87,7 @@ def kernel_entries():
     for fam in spaces.TC_FAMILIES:
         for t in spaces.enumerate_tuples(fam, spaces.B200_CAPS, spaces.PROFILE_B200_TC):
             _, bm, bn, bk, tm, tn, uk = t
-            kind = "ag::tc::KIND_TF32" if fam == "tf32" else "ag::tc::KIND_BF16"
+            kind = {"tf32": "ag::tc::KIND_TF32", "bf16": "ag::tc::KIND_BF16", "tf32x3": "ag::tc::KIND_TF32X3"}[fam]
             out.append((FAMILY_CODE[fam], 0, bm, bn, bk, tm, tn, uk,
                         f"&ag::tc::launch_tc<{kind}, {bn}, {tm}, {bm // 128}>", 3.0))
     for dcode, ctype in ((0, "float"), (1, "double")):

@@ -18,6 +18,7 @@
 #include "kernels.cuh"
 #include "launch.cuh"
 #include "registry.h"
+#include "hoststage.h"
 #include "skinny.cuh"
 #include "tc_kernels.cuh"
 
@@ -134,6 +135,7 @@ std::string config_str(const ag_config& c) {
                       : c.family == AG_FAMILY_SPLITK ? "splitk"
                       : c.family == AG_FAMILY_TF32   ? "tf32"
                       : c.family == AG_FAMILY_BF16   ? "bf16"
+                      : c.family == AG_FAMILY_TF32X3 ? "tf32x3"
                       : c.family == AG_FAMILY_TMA    ? "tma"
                       : c.family == AG_FAMILY_SKINNY_N ? "skinny_n"
                       : c.family == AG_FAMILY_SKINNY_M ? "skinny_m"
@@ -368,6 +370,7 @@ struct HostPipe {
     std::vector<cudaEvent_t> tev;  // timing events around each panel's family path
     void* scratch = nullptr;       // ag_device_scratch: grow-only, per thread and device
     size_t scratch_bytes = 0;
+    ag::hoststage::Ring rin, rout;  // pageable staging (AG_HOST_STAGE), allocated on first use
     void* pinned = nullptr;        // small-call staging (cudaHostAlloc), grow-only
     size_t pinned_bytes = 0;
     void* pinned_buffer(size_t bytes) {
@@ -500,16 +503,18 @@ const char* ag_version(void) { return "adaptgemm-b200 0.1.0 (sm_100a)"; }
 int ag_is_legal(const ag_config* c, const ag_caps* caps) {
     if (!c || !caps) return 0;
     if (std::min({c->bm, c->bn, c->bk, c->tm, c->tn, c->uk}) < 1) return 0;
-    if (c->family == AG_FAMILY_TF32 || c->family == AG_FAMILY_BF16) {
+    if (c->family == AG_FAMILY_TF32 || c->family == AG_FAMILY_BF16 || c->family == AG_FAMILY_TF32X3) {
         // spaces.is_legal_tuple: tensor-core resources are TMEM and the
         // stage ring, not the CUDA-core register / tile caps
-        const int bk = c->family == AG_FAMILY_TF32 ? 32 : 64;
-        const int chunk = c->family == AG_FAMILY_TF32 ? 32 : 64;
+        const int bk = c->family == AG_FAMILY_BF16 ? 64 : 32;
+        const int chunk = c->family == AG_FAMILY_BF16 ? 64 : 32;
+        const int parts = c->family == AG_FAMILY_TF32X3 ? 2 : 1;
         if ((c->bm != 128 && c->bm != 256) || c->bk != bk || c->tn != 1 || c->uk != 1) return 0;
         if (c->bn % 32 || c->bn < 32 || c->bn > 256 || c->tm < 2 || c->tm > 8) return 0;
         const int ctas = c->bm / 128;
         if (ctas == 2 && (c->bn / 2) % chunk) return 0;
-        const int64_t smem = (int64_t)c->tm * (128 + c->bn / ctas) * 128 + 1024 + (int64_t)ag::tc::EPI_BYTES + 256;
+        const int64_t smem =
+            (int64_t)c->tm * parts * (128 + c->bn / ctas) * 128 + 1024 + (int64_t)ag::tc::EPI_BYTES + 256;
         return smem <= 227 * 1024;
     }
     if (c->family == AG_FAMILY_SKINNY_N || c->family == AG_FAMILY_SKINNY_M) {
@@ -564,6 +569,8 @@ size_t ag_workspace_bytes(const ag_shape* s, const ag_config* c, int dtype) {
     if (!s || !c || c->family == AG_FAMILY_DIRECT || !in_range(*c)) return 0;
     if (c->family == AG_FAMILY_TF32) return ag::tc::workspace_bytes<ag::tc::KIND_TF32>(s->m, s->n, s->k, s->trans_a, s->trans_b);
     if (c->family == AG_FAMILY_BF16) return ag::tc::workspace_bytes<ag::tc::KIND_BF16>(s->m, s->n, s->k, s->trans_a, s->trans_b);
+    if (c->family == AG_FAMILY_TF32X3)
+        return ag::tc::workspace_bytes<ag::tc::KIND_TF32X3>(s->m, s->n, s->k, s->trans_a, s->trans_b);
     if (c->family == AG_FAMILY_SKINNY_N || c->family == AG_FAMILY_SKINNY_M) {
         // no workspace on the skinny kernels; sized for their split-K fallback
         // (transposed / unaligned / float64 calls: skinny.cuh fallback())
@@ -707,6 +714,11 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
         if (h.reads_c) locks.lock(C, s->m, ldc, s->n, h.elem);
         locks.lock(out, s->m, ldo, s->n, h.elem);
     }
+    // AG_HOST_STAGE: pageable buffers cross through the pinned rings (host
+    // copies in parallel with the DMA and the kernels); pinned ones as DMA
+    const bool stage = (flags & AG_HOST_STAGE) && t_pipe.rin.ok() && t_pipe.rout.ok();
+    const bool pin_a = !stage || ag::hoststage::is_pinned(A), pin_b = !stage || ag::hoststage::is_pinned(B);
+    const bool pin_c = !stage || !h.reads_c || ag::hoststage::is_pinned(C), pin_o = !stage || ag::hoststage::is_pinned(out);
     cudaStream_t in = t_pipe.s[0], run = t_pipe.s[1], back = t_pipe.s[2];
     char* base = static_cast<char*>(dev);
     char *dA = base + h.offA, *dB = base + h.offB, *dC = base + h.offC, *dO = base + h.offO;
@@ -715,6 +727,21 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
     const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
     cudaError_t ce = cudaSuccess;
     auto ok = [&](cudaError_t x) { if (x != cudaSuccess && ce == cudaSuccess) ce = x; };
+    // rows x width bytes host -> device on `in` / device -> host on `back`
+    auto put = [&](bool pinned, char* d, int64_t dp, const void* hsrc, int64_t hp, int64_t width, int64_t rows) {
+        if (pinned) {
+            ok(copy2d(d, dp, hsrc, hp, width, rows, H2D, in));
+        } else {
+            ok(ag::hoststage::h2d(t_pipe.rin, {static_cast<char*>(const_cast<void*>(hsrc)), hp, d, dp, width, rows}, in));
+        }
+    };
+    auto get = [&](bool pinned, void* hdst, int64_t hp, char* d, int64_t dp, int64_t width, int64_t rows) {
+        if (pinned) {
+            ok(copy2d(hdst, hp, d, dp, width, rows, D2H, back));
+        } else {
+            ok(ag::hoststage::d2h(t_pipe.rout, {static_cast<char*>(hdst), hp, d, dp, width, rows}, back));
+        }
+    };
     // the caller's stream may still be writing the host buffers' producers
     cudaEvent_t start = t_pipe.event(0);
     if (!start) return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
@@ -722,10 +749,20 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
     ok(cudaStreamWaitEvent(in, start, 0));
     // the operand that is not split crosses once, first
     if (h.by_rows) {
-        ok(copy2d(dB, h.cb * e, B, ldb * e, h.cb * e, h.rb, H2D, in));
+        put(pin_b, dB, h.cb * e, B, ldb * e, h.cb * e, h.rb);
     } else {
-        ok(copy2d(dA, h.ca * e, A, lda * e, h.ca * e, h.ra, H2D, in));
+        put(pin_a, dA, h.ca * e, A, lda * e, h.ca * e, h.ra);
     }
+    // panel p's output back to the host (after its family path)
+    auto drain = [&](int p) {
+        const int64_t x0 = (int64_t)p * h.chunk, w = std::min(h.chunk, h.extent - x0);
+        ok(cudaStreamWaitEvent(back, t_pipe.event(2 + 2 * p), 0));
+        if (h.by_rows) {
+            get(pin_o, static_cast<char*>(out) + x0 * ldo * e, ldo * e, dO + x0 * N * e, N * e, N * e, w);
+        } else {
+            get(pin_o, static_cast<char*>(out) + x0 * e, ldo * e, dO + x0 * e, N * e, w * e, M);
+        }
+    };
     for (int p = 0; p < h.panels; ++p) {
         const int64_t x0 = (int64_t)p * h.chunk, w = std::min(h.chunk, h.extent - x0);
         cudaEvent_t ein = t_pipe.event(1 + 2 * p), edone = t_pipe.event(2 + 2 * p);
@@ -736,36 +773,31 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
         int64_t pla, plb;
         if (h.by_rows) {  // rows x0 .. x0+w of op(A), C, out
             if (!s->trans_a) {
-                ok(copy2d(dA + x0 * h.ca * e, h.ca * e, static_cast<const char*>(A) + x0 * lda * e, lda * e,
-                          h.ca * e, w, H2D, in));
+                put(pin_a, dA + x0 * h.ca * e, h.ca * e, static_cast<const char*>(A) + x0 * lda * e, lda * e, h.ca * e, w);
                 pa = dA + x0 * h.ca * e;
             } else {  // stored K x M: a column block
-                ok(copy2d(dA + x0 * e, h.ca * e, static_cast<const char*>(A) + x0 * e, lda * e, w * e, h.ra, H2D, in));
+                put(pin_a, dA + x0 * e, h.ca * e, static_cast<const char*>(A) + x0 * e, lda * e, w * e, h.ra);
                 pa = dA + x0 * e;
             }
             pla = h.ca;
             pb = dB;
             plb = h.cb;
-            if (h.reads_c)
-                ok(copy2d(dC + x0 * N * e, N * e, static_cast<const char*>(C) + x0 * ldc * e, ldc * e, N * e, w, H2D,
-                          in));
+            if (h.reads_c) put(pin_c, dC + x0 * N * e, N * e, static_cast<const char*>(C) + x0 * ldc * e, ldc * e, N * e, w);
             pc = h.reads_c ? (const void*)(dC + x0 * N * e) : (const void*)(dO + x0 * N * e);
             po = dO + x0 * N * e;
             ps.m = w;
         } else {  // columns x0 .. x0+w of op(B), C, out
             if (!s->trans_b) {  // stored K x N: a column block
-                ok(copy2d(dB + x0 * e, h.cb * e, static_cast<const char*>(B) + x0 * e, ldb * e, w * e, h.rb, H2D, in));
+                put(pin_b, dB + x0 * e, h.cb * e, static_cast<const char*>(B) + x0 * e, ldb * e, w * e, h.rb);
                 pb = dB + x0 * e;
             } else {  // stored N x K: rows
-                ok(copy2d(dB + x0 * h.cb * e, h.cb * e, static_cast<const char*>(B) + x0 * ldb * e, ldb * e,
-                          h.cb * e, w, H2D, in));
+                put(pin_b, dB + x0 * h.cb * e, h.cb * e, static_cast<const char*>(B) + x0 * ldb * e, ldb * e, h.cb * e, w);
                 pb = dB + x0 * h.cb * e;
             }
             plb = h.cb;
             pa = dA;
             pla = h.ca;
-            if (h.reads_c)
-                ok(copy2d(dC + x0 * e, N * e, static_cast<const char*>(C) + x0 * e, ldc * e, w * e, M, H2D, in));
+            if (h.reads_c) put(pin_c, dC + x0 * e, N * e, static_cast<const char*>(C) + x0 * e, ldc * e, w * e, M);
             pc = h.reads_c ? (const void*)(dC + x0 * e) : (const void*)(dO + x0 * e);
             po = dO + x0 * e;
             ps.n = w;
@@ -784,13 +816,10 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
             return r;
         }
         ok(cudaEventRecord(edone, run));
-        ok(cudaStreamWaitEvent(back, edone, 0));
-        if (h.by_rows) {
-            ok(copy2d(static_cast<char*>(out) + x0 * ldo * e, ldo * e, dO + x0 * N * e, N * e, N * e, w, D2H, back));
-        } else {
-            ok(copy2d(static_cast<char*>(out) + x0 * e, ldo * e, dO + x0 * e, N * e, w * e, M, D2H, back));
-        }
+        // the previous panel's output drains while this panel computes
+        if (p >= 1) drain(p - 1);
     }
+    drain(h.panels - 1);
     ok(cudaStreamSynchronize(back));
     ok(cudaStreamSynchronize(run));
     ok(cudaStreamSynchronize(in));

@@ -232,7 +232,7 @@ static PyObject* fp_execute(PyObject* self, PyObject* const* args, Py_ssize_t na
         int rc;
         Py_BEGIN_ALLOW_THREADS
         rc = ag_gemm_host_ex(&s, &c, &k, a.code, a.view.buf, lda, b.view.buf, ldb, cc.view.buf, ldc, o.view.buf,
-                             ldo, NULL, 0, 0, AG_HOST_REGISTER, NULL, &secs);
+                             ldo, NULL, 0, 0, AG_HOST_STAGE, NULL, &secs);
         Py_END_ALLOW_THREADS
         if (rc) {
             Py_DECREF(dst);

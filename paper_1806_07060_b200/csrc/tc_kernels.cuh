@@ -35,6 +35,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
 #include <atomic>
 #include <mutex>
 
@@ -47,6 +48,7 @@ namespace tc {
 
 constexpr int KIND_TF32 = 0;
 constexpr int KIND_BF16 = 1;
+constexpr int KIND_TF32X3 = 2;  // fp32-accurate: 3 tf32 products over hi / lo operand parts
 constexpr int BM = 128;          // UMMA M (cta_group::1): TMEM lane = output row
 constexpr int ROW_BYTES = 128;   // one K block = one 128-byte swizzle row
 constexpr int THREADS = 192;     // producer warp, MMA warp, 4 epilogue warps
@@ -61,6 +63,7 @@ template <> struct Elem<KIND_TF32> {
     static constexpr int UMMA_K = 8;
     static constexpr uint32_t FMT = 2;        // TF32
     static constexpr CUtensorMapDataType TMA = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    static constexpr int PARTS = 1;           // operand parts staged per K block
 };
 template <> struct Elem<KIND_BF16> {
     typedef __nv_bfloat16 T;
@@ -68,6 +71,17 @@ template <> struct Elem<KIND_BF16> {
     static constexpr int UMMA_K = 16;
     static constexpr uint32_t FMT = 1;        // BF16
     static constexpr CUtensorMapDataType TMA = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    static constexpr int PARTS = 1;
+};
+// 3xTF32: x = hi + lo with hi = x with its low 13 mantissa bits cleared (the
+// bits a tf32 MMA reads) and lo = x - hi (exact in fp32, |lo| < 2^-10 |x|).
+// a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi: the dropped a_lo.b_lo and the
+// tf32 truncation of the lo parts are below 2^-20 |a||b| per product, so the
+// result meets the fp32 families' RF <= 1e-5 contract on the tensor pipe.
+// A stage holds [hi | lo] of each operand; the MMA issuer runs 3 tf32 MMAs
+// per K step into the same TMEM accumulator.
+template <> struct Elem<KIND_TF32X3> : Elem<KIND_TF32> {
+    static constexpr int PARTS = 2;
 };
 
 // ---------------------------------------------------------------- device PTX
@@ -132,7 +146,7 @@ __host__ __device__ constexpr uint32_t instr_desc(int m, int n, int a_mn, int b_
 
 template <int KIND>
 __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    if constexpr (KIND == KIND_TF32) {
+    if constexpr (KIND != KIND_BF16) {
         asm volatile(
             "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
             " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
@@ -198,9 +212,9 @@ constexpr uint32_t tmem_cols() {
 constexpr int EPI_LD = 36;
 constexpr size_t EPI_BYTES = 4 * 32 * EPI_LD * sizeof(float);
 
-template <int BN, int STAGES, int CTAS>
+template <int BN, int STAGES, int CTAS, int PARTS = 1>
 constexpr size_t smem_bytes() {
-    return 1024 + (size_t)STAGES * (BM + BN / CTAS) * ROW_BYTES + EPI_BYTES + 256;
+    return 1024 + (size_t)STAGES * PARTS * (BM + BN / CTAS) * ROW_BYTES + EPI_BYTES + 256;
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -225,7 +239,7 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
 template <int KIND>
 __device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t acc) {
-    if constexpr (KIND == KIND_TF32) {
+    if constexpr (KIND != KIND_BF16) {
         asm volatile(
             "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
             " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
@@ -258,17 +272,19 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) 
 // 128 output rows.  Per SM this halves the B traffic of a 128 x BN tile.
 template <int KIND, int BN, int STAGES, int CTAS>
 __global__ void __launch_bounds__(THREADS, 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p) {
+tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+               const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo, TcParams p) {
     constexpr int BK = Elem<KIND>::BK;
+    constexpr int PARTS = Elem<KIND>::PARTS;  // [hi | lo] per operand and stage for 3xTF32
     constexpr int BNC = BN / CTAS;  // B rows (N) staged by each CTA
-    constexpr uint32_t A_BYTES = BM * ROW_BYTES, B_BYTES = BNC * ROW_BYTES;
-    constexpr uint32_t STAGE_TX = (A_BYTES + B_BYTES) * CTAS;
+    constexpr uint32_t A_BYTES = BM * ROW_BYTES, B_BYTES = BNC * ROW_BYTES;  // one part
+    constexpr uint32_t STAGE_TX = (A_BYTES + B_BYTES) * CTAS * PARTS;
     constexpr uint32_t TMEM_COLS = tmem_cols<BN>();
     constexpr int K_STEPS = BK / Elem<KIND>::UMMA_K;
     constexpr int CH = ROW_BYTES / (int)sizeof(typename Elem<KIND>::T);  // elements per 128-byte MN chunk
     constexpr uint32_t CHUNK_BYTES = BK * ROW_BYTES;                      // one MN chunk of one stage
-    constexpr uint32_t MN_SBO = KIND == KIND_TF32 ? 512 : 1024;           // see sw128_desc
-    constexpr uint32_t MN_LAYOUT = KIND == KIND_TF32 ? 1 : 2;
+    constexpr uint32_t MN_SBO = KIND != KIND_BF16 ? 512 : 1024;           // see sw128_desc
+    constexpr uint32_t MN_LAYOUT = KIND != KIND_BF16 ? 1 : 2;
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "UMMA N is 16..256; the epilogue drains 32 columns");
     static_assert(CTAS == 1 || CTAS == 2, "one CTA or a CTA pair");
     static_assert(BNC % CH == 0 || CTAS == 1, "pair tiles split B into whole 128-byte chunks");
@@ -277,10 +293,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     // 1024-byte aligned (128-byte swizzle atoms); offset from the shared-window
     // address so the pointer stays in the shared space (LDS/STS, not generic)
     uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * A_BYTES;
-    float* sEpi = reinterpret_cast<float*>(sB + STAGES * B_BYTES);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES + EPI_BYTES);
+    uint8_t* sA = smem;                              // [STAGES][PARTS][A_BYTES]
+    uint8_t* sB = smem + STAGES * PARTS * A_BYTES;   // [STAGES][PARTS][B_BYTES]
+    float* sEpi = reinterpret_cast<float*>(sB + STAGES * PARTS * B_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * PARTS * B_BYTES + EPI_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + ACC_STAGES;
@@ -292,6 +308,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+        if constexpr (PARTS == 2) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapAlo)) : "memory");
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapBlo)) : "memory");
+        }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -343,40 +363,48 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 const int m0 = tm * BM * CTAS + (int)rank * BM, n0 = tn * BN + (int)rank * BNC;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* a = sA + stage * A_BYTES;
-                    uint8_t* b = sB + stage * B_BYTES;
                     if constexpr (CTAS == 1) {
                         mbar_expect_tx(&full[stage], STAGE_TX);
-                        if (!p.a_mn) {
-                            tma_load_2d(a, &mapA, &full[stage], kb * BK, m0);
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < BM / CH; ++c)
-                                tma_load_2d(a + c * CHUNK_BYTES, &mapA, &full[stage], m0 + c * CH, kb * BK);
-                        }
-                        if (!p.b_mn) {
-                            tma_load_2d(b, &mapB, &full[stage], kb * BK, n0);
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < BNC / CH; ++c)
-                                tma_load_2d(b + c * CHUNK_BYTES, &mapB, &full[stage], n0 + c * CH, kb * BK);
-                        }
                     } else {
-                        const uint32_t bar = smem_addr(&full[stage]) & 0xFEFFFFFFu;  // leader's barrier
                         if (rank == 0) mbar_expect_tx(&full[stage], STAGE_TX);
-                        if (!p.a_mn) {
-                            tma_load_2d_pair(a, &mapA, bar, kb * BK, m0);
-                        } else {
+                    }
 #pragma unroll
-                            for (int c = 0; c < BM / CH; ++c)
-                                tma_load_2d_pair(a + c * CHUNK_BYTES, &mapA, bar, m0 + c * CH, kb * BK);
-                        }
-                        if (!p.b_mn) {
-                            tma_load_2d_pair(b, &mapB, bar, kb * BK, n0);
-                        } else {
+                    for (int part = 0; part < PARTS; ++part) {
+                        uint8_t* a = sA + (stage * PARTS + part) * A_BYTES;
+                        uint8_t* b = sB + (stage * PARTS + part) * B_BYTES;
+                        const CUtensorMap* ma = part ? &mapAlo : &mapA;
+                        const CUtensorMap* mb = part ? &mapBlo : &mapB;
+                        if constexpr (CTAS == 1) {
+                            if (!p.a_mn) {
+                                tma_load_2d(a, ma, &full[stage], kb * BK, m0);
+                            } else {
 #pragma unroll
-                            for (int c = 0; c < BNC / CH; ++c)
-                                tma_load_2d_pair(b + c * CHUNK_BYTES, &mapB, bar, n0 + c * CH, kb * BK);
+                                for (int c = 0; c < BM / CH; ++c)
+                                    tma_load_2d(a + c * CHUNK_BYTES, ma, &full[stage], m0 + c * CH, kb * BK);
+                            }
+                            if (!p.b_mn) {
+                                tma_load_2d(b, mb, &full[stage], kb * BK, n0);
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < BNC / CH; ++c)
+                                    tma_load_2d(b + c * CHUNK_BYTES, mb, &full[stage], n0 + c * CH, kb * BK);
+                            }
+                        } else {
+                            const uint32_t bar = smem_addr(&full[stage]) & 0xFEFFFFFFu;  // leader's barrier
+                            if (!p.a_mn) {
+                                tma_load_2d_pair(a, ma, bar, kb * BK, m0);
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < BM / CH; ++c)
+                                    tma_load_2d_pair(a + c * CHUNK_BYTES, ma, bar, m0 + c * CH, kb * BK);
+                            }
+                            if (!p.b_mn) {
+                                tma_load_2d_pair(b, mb, bar, kb * BK, n0);
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < BNC / CH; ++c)
+                                    tma_load_2d_pair(b + c * CHUNK_BYTES, mb, bar, n0 + c * CH, kb * BK);
+                            }
                         }
                     }
                     if (++stage == STAGES) {
@@ -397,19 +425,34 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a0 = smem_addr(sA + stage * A_BYTES), b0 = smem_addr(sB + stage * B_BYTES);
+                    const uint32_t a0 = smem_addr(sA + stage * PARTS * A_BYTES);
+                    const uint32_t b0 = smem_addr(sB + stage * PARTS * B_BYTES);
+                    auto adesc = [&](uint32_t base, int k) {
+                        return p.a_mn ? sw128_desc(base + k * Elem<KIND>::UMMA_K * ROW_BYTES, CHUNK_BYTES, MN_SBO,
+                                                   MN_LAYOUT)
+                                      : sw128_desc(base + k * 32);
+                    };
+                    auto bdesc = [&](uint32_t base, int k) {
+                        return p.b_mn ? sw128_desc(base + k * Elem<KIND>::UMMA_K * ROW_BYTES, CHUNK_BYTES, MN_SBO,
+                                                   MN_LAYOUT)
+                                      : sw128_desc(base + k * 32);
+                    };
+                    auto mma = [&](uint64_t ad, uint64_t bd, uint32_t accumulate) {
+                        if constexpr (CTAS == 1) {
+                            umma<KIND>(d, ad, bd, p.idesc, accumulate);
+                        } else {
+                            umma_pair<KIND>(d, ad, bd, p.idesc, accumulate);
+                        }
+                    };
 #pragma unroll
                     for (int k = 0; k < K_STEPS; ++k) {
-                        const uint64_t ad =
-                            p.a_mn ? sw128_desc(a0 + k * Elem<KIND>::UMMA_K * ROW_BYTES, CHUNK_BYTES, MN_SBO, MN_LAYOUT)
-                                   : sw128_desc(a0 + k * 32);
-                        const uint64_t bd =
-                            p.b_mn ? sw128_desc(b0 + k * Elem<KIND>::UMMA_K * ROW_BYTES, CHUNK_BYTES, MN_SBO, MN_LAYOUT)
-                                   : sw128_desc(b0 + k * 32);
-                        if constexpr (CTAS == 1) {
-                            umma<KIND>(d, ad, bd, p.idesc, (kb | k) != 0);
+                        const uint64_t ad = adesc(a0, k), bd = bdesc(b0, k);
+                        if constexpr (PARTS == 2) {  // small products first: a_lo.b_hi, a_hi.b_lo, a_hi.b_hi
+                            mma(adesc(a0 + A_BYTES, k), bd, (kb | k) != 0);
+                            mma(ad, bdesc(b0 + B_BYTES, k), 1u);
+                            mma(ad, bd, 1u);
                         } else {
-                            umma_pair<KIND>(d, ad, bd, p.idesc, (kb | k) != 0);
+                            mma(ad, bd, (kb | k) != 0);
                         }
                     }
                     if constexpr (CTAS == 1) {
@@ -555,7 +598,8 @@ __device__ __forceinline__ void store4(__nv_bfloat16* d, float a, float b, float
 __device__ __forceinline__ void store1(float* d, float a) { *d = a; }
 __device__ __forceinline__ void store1(__nv_bfloat16* d, float a) { *d = __float2bfloat16_rn(a); }
 
-// One staging job: dst (rows x cols, ld_dst) = src converted to the MMA type.
+// One staging job: dst (rows x cols, ld_dst) = src converted to the MMA type,
+// or (lo = 1, fp32 only) the 3xTF32 low part x - hi(x).
 template <typename D>
 struct ConvertJob {
     D* dst;
@@ -564,7 +608,28 @@ struct ConvertJob {
     i64 ld_src;
     i64 rows, cols, quads;  // quads = rows * ceil(cols / 4); 0 = no job
     int vec;                // 16-byte source rows: one LDG.128 per quad
+    int lo;                 // write x - hi(x) (3xTF32 low part)
 };
+// every staging job of one call (up to hi / lo of A and B), one launch
+template <typename D>
+struct ConvertJobs {
+    ConvertJob<D> j[4];
+};
+
+// 3xTF32 split: hi = the bits a tf32 MMA reads (low 13 mantissa bits
+// cleared), lo = x - hi, exact in fp32
+__host__ __device__ __forceinline__ float tf32_hi(float x) {
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+#else
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u &= 0xFFFFE000u;
+    std::memcpy(&x, &u, 4);
+    return x;
+#endif
+}
+__host__ __device__ __forceinline__ float tf32_lo(float x) { return x - tf32_hi(x); }
 
 // Both operands' staging in ONE launch: a flat grid-stride over the
 // (row, 4-column quad) space of job a then job b, 4 quads per thread per step
@@ -584,26 +649,35 @@ __device__ __forceinline__ void convert_quad(const ConvertJob<D>& j, i64 q) {
         } else {
             v = make_float4(__ldcs(sp), __ldcs(sp + 1), __ldcs(sp + 2), __ldcs(sp + 3));
         }
+        if (j.lo) v = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
         store4(dp, v.x, v.y, v.z, v.w, true);
     } else {
-        for (i64 k = c; k < j.cols; ++k) store1(j.dst + r * j.ld_dst + k, j.src[r * j.ld_src + k]);
+        for (i64 k = c; k < j.cols; ++k) {
+            const float x = j.src[r * j.ld_src + k];
+            store1(j.dst + r * j.ld_dst + k, j.lo ? tf32_lo(x) : x);
+        }
     }
 }
 template <typename D>
 __global__ void __launch_bounds__(256)
-tc_convert_kernel(const ConvertJob<D> a, const ConvertJob<D> b) {
+tc_convert_kernel(const ConvertJobs<D> jobs) {
     // let the tc_gemm launch (programmatic dependent launch) start its setup
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    const i64 total = a.quads + b.quads;
+    const i64 q1 = jobs.j[0].quads, q2 = q1 + jobs.j[1].quads, q3 = q2 + jobs.j[2].quads;
+    const i64 total = q3 + jobs.j[3].quads;
     const i64 stride = (i64)gridDim.x * blockDim.x;
     for (i64 q0 = (i64)blockIdx.x * blockDim.x + threadIdx.x; q0 < total; q0 += 4 * stride) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const i64 q = q0 + u * stride;
-            if (q < a.quads) {
-                convert_quad(a, q);
+            if (q < q1) {
+                convert_quad(jobs.j[0], q);
+            } else if (q < q2) {
+                convert_quad(jobs.j[1], q - q1);
+            } else if (q < q3) {
+                convert_quad(jobs.j[2], q - q2);
             } else if (q < total) {
-                convert_quad(b, q - a.quads);
+                convert_quad(jobs.j[3], q - q3);
             }
         }
     }
@@ -643,7 +717,7 @@ inline bool make_map(CUtensorMap* map, const void* base, i64 rows, i64 cols, i64
     cuuint32_t estr[2] = {1, 1};
     // 32-bit MN-major tiles: 32-byte swizzle atoms (see sw128_desc)
     const CUtensorMapSwizzle swz =
-        (KIND == KIND_TF32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+        (KIND != KIND_BF16 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
     CUresult r = fn(map, Elem<KIND>::TMA, 2, const_cast<void*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -667,22 +741,24 @@ inline i64 staged_ld(i64 cols) {
 }
 
 // [A staging | B staging], each 1024-byte aligned: converted (bf16) or
-// re-strided (tf32, only used when a row stride is not 16-byte aligned)
+// re-strided (tf32, only used when a row stride is not 16-byte aligned);
+// 3xTF32 adds [A lo | B lo] after them
+template <int KIND>
+inline size_t staged_bytes(i64 rows, i64 cols) {
+    return (size_t)round_up_i(rows * staged_ld<KIND>(cols) * (i64)sizeof(typename Elem<KIND>::T), 1024);
+}
 template <int KIND>
 inline size_t workspace_bytes(i64 M, i64 N, i64 K, int ta, int tb) {
-    typedef typename Elem<KIND>::T T;
     const OperandLayout a = layout_a(M, K, ta), b = layout_b(N, K, tb);
-    return (size_t)round_up_i(a.rows * staged_ld<KIND>(a.cols) * (i64)sizeof(T), 1024) +
-           (size_t)round_up_i(b.rows * staged_ld<KIND>(b.cols) * (i64)sizeof(T), 1024);
+    return (size_t)Elem<KIND>::PARTS * (staged_bytes<KIND>(a.rows, a.cols) + staged_bytes<KIND>(b.rows, b.cols));
 }
 
-template <int KIND>
-inline int launch_converts(const ConvertJob<typename Elem<KIND>::T>& a, const ConvertJob<typename Elem<KIND>::T>& b,
-                           cudaStream_t stream) {
-    const i64 total = a.quads + b.quads;
+template <typename T>
+inline int launch_converts(const ConvertJobs<T>& jobs, cudaStream_t stream) {
+    const i64 total = jobs.j[0].quads + jobs.j[1].quads + jobs.j[2].quads + jobs.j[3].quads;
     if (total == 0) return AG_OK;
     const unsigned blocks = (unsigned)std::max<i64>(1, std::min<i64>((total + 1023) / 1024, (i64)sm_count() * 8));
-    tc_convert_kernel<typename Elem<KIND>::T><<<blocks, 256, 0, stream>>>(a, b);
+    tc_convert_kernel<T><<<blocks, 256, 0, stream>>>(jobs);
     return cudaGetLastError() == cudaSuccess ? AG_OK : AG_ERR_CUDA;
 }
 
@@ -697,10 +773,10 @@ inline int tc_fail(const GemmCall& c, int code, const char* msg) {
 // conversion job (quads = 0 when the operand is read in place).
 template <int KIND>
 inline ConvertJob<typename Elem<KIND>::T> plan_operand(const float* src, i64 ld_src, OperandLayout lay, void* ws,
-                                                       const void** base, i64* ld) {
+                                                       const void** base, i64* ld, int lo = 0) {
     typedef typename Elem<KIND>::T T;
     ConvertJob<T> j{};
-    if (KIND == KIND_TF32 && ld_src % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+    if (KIND != KIND_BF16 && !lo && ld_src % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
         *base = src;
         *ld = ld_src;
         return j;
@@ -715,6 +791,7 @@ inline ConvertJob<typename Elem<KIND>::T> plan_operand(const float* src, i64 ld_
     j.cols = lay.cols;
     j.quads = lay.rows * ((lay.cols + 3) / 4);
     j.vec = (ld_src % 4 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+    j.lo = lo;
     return j;
 }
 
@@ -731,25 +808,41 @@ int launch_tc(const GemmCall& c) {
         return tc_fail(c, AG_ERR_SHAPE, "problem too large for the tensor-core grid");
     const OperandLayout la = layout_a(M, K, c.ta), lb = layout_b(N, K, c.tb);
     const size_t need = workspace_bytes<KIND>(M, N, K, c.ta, c.tb);
-    if (KIND == KIND_BF16 && (c.ws_bytes < need || c.ws == nullptr))
+    if ((KIND == KIND_BF16 || Elem<KIND>::PARTS == 2) && (c.ws_bytes < need || c.ws == nullptr))
         return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
+    const size_t a_st = staged_bytes<KIND>(la.rows, la.cols), b_st = staged_bytes<KIND>(lb.rows, lb.cols);
     char* wsA = static_cast<char*>(c.ws);
-    char* wsB = wsA ? wsA + round_up_i(la.rows * staged_ld<KIND>(la.cols) * (i64)sizeof(T), 1024) : nullptr;
-    const void *baseA = nullptr, *baseB = nullptr;
-    i64 ldA = 0, ldB = 0;
-    const auto jobA = plan_operand<KIND>(static_cast<const float*>(c.A), c.lda, la, wsA, &baseA, &ldA);
-    const auto jobB = plan_operand<KIND>(static_cast<const float*>(c.B), c.ldb, lb, wsB, &baseB, &ldB);
-    if ((jobA.quads || jobB.quads) && (c.ws_bytes < need || c.ws == nullptr))
+    char* wsB = wsA ? wsA + a_st : nullptr;
+    const void *baseA = nullptr, *baseB = nullptr, *baseAlo = nullptr, *baseBlo = nullptr;
+    i64 ldA = 0, ldB = 0, ldAlo = 0, ldBlo = 0;
+    ConvertJobs<T> jobs{};
+    jobs.j[0] = plan_operand<KIND>(static_cast<const float*>(c.A), c.lda, la, wsA, &baseA, &ldA);
+    jobs.j[1] = plan_operand<KIND>(static_cast<const float*>(c.B), c.ldb, lb, wsB, &baseB, &ldB);
+    if constexpr (Elem<KIND>::PARTS == 2) {  // 3xTF32: the lo parts always stage (hi is read in place when aligned)
+        jobs.j[2] = plan_operand<KIND>(static_cast<const float*>(c.A), c.lda, la, wsA + a_st + b_st, &baseAlo, &ldAlo, 1);
+        jobs.j[3] = plan_operand<KIND>(static_cast<const float*>(c.B), c.ldb, lb, wsA + 2 * a_st + b_st, &baseBlo,
+                                       &ldBlo, 1);
+    }
+    const bool staged = jobs.j[0].quads || jobs.j[1].quads || jobs.j[2].quads || jobs.j[3].quads;
+    if (staged && (c.ws_bytes < need || c.ws == nullptr))
         return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
-    if (launch_converts<KIND>(jobA, jobB, c.stream) != AG_OK) return tc_fail(c, AG_ERR_CUDA, "staging of the operands failed");
+    if (launch_converts<T>(jobs, c.stream) != AG_OK) return tc_fail(c, AG_ERR_CUDA, "staging of the operands failed");
 
     // A: K-major unless transA; B: MN-major unless transB.  Boxes are per
     // CTA: 128 rows of A, BN / CTAS rows of B.
     const int a_mn = c.ta ? 1 : 0, b_mn = c.tb ? 0 : 1;
-    CUtensorMap mapA, mapB;
+    CUtensorMap mapA, mapB, mapAlo, mapBlo;
     if (!make_map<KIND>(&mapA, baseA, la.rows, la.cols, ldA, a_mn, BM) ||
         !make_map<KIND>(&mapB, baseB, lb.rows, lb.cols, ldB, b_mn, BN / CTAS))
         return tc_fail(c, AG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    if constexpr (Elem<KIND>::PARTS == 2) {
+        if (!make_map<KIND>(&mapAlo, baseAlo, la.rows, la.cols, ldAlo, a_mn, BM) ||
+            !make_map<KIND>(&mapBlo, baseBlo, lb.rows, lb.cols, ldBlo, b_mn, BN / CTAS))
+            return tc_fail(c, AG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    } else {
+        mapAlo = mapA;
+        mapBlo = mapB;
+    }
 
     TcParams p;
     p.M = (int)M;
@@ -773,7 +866,7 @@ int launch_tc(const GemmCall& c) {
 
     // >= 116 KB of shared memory keeps one CTA per SM, so a CTA never waits
     // on another CTA's TMEM allocation
-    const size_t smem = std::max<size_t>(smem_bytes<BN, STAGES, CTAS>(), 116 * 1024);
+    const size_t smem = std::max<size_t>(smem_bytes<BN, STAGES, CTAS, Elem<KIND>::PARTS>(), 116 * 1024);
     if (smem > 227 * 1024) return tc_fail(c, AG_ERR_CONFIG, "config exceeds 227 KB shared memory per CTA");
     auto kernel = tc_gemm_kernel<KIND, BN, STAGES, CTAS>;
     static SmemGrant granted;  // per device: the attribute applies to the current device only
@@ -796,8 +889,8 @@ int launch_tc(const GemmCall& c) {
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (jobA.quads || jobB.quads) ? 2 : 1;
-    if (cudaLaunchKernelEx(&cfg, kernel, mapA, mapB, p) != cudaSuccess)
+    cfg.numAttrs = staged ? 2 : 1;
+    if (cudaLaunchKernelEx(&cfg, kernel, mapA, mapB, mapAlo, mapBlo, p) != cudaSuccess)
         return tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
     return cudaGetLastError() == cudaSuccess ? AG_OK : tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
 }

@@ -48,6 +48,10 @@ class KernelFamily(str, Enum):
     SKINNY_N / SKINNY_M stream the big operand of a GEMM whose N (resp. M)
     is small, K split over the CTAs of a cluster (csrc/skinny.cuh; B200
     profiles only).
+    TF32X3 is fp32-accurate GEMM on the tensor pipe: each operand split as
+    hi + lo (hi = its tf32 bits), three tf32 MMAs (hi.hi + hi.lo + lo.hi)
+    into one fp32 TMEM accumulator; it meets the fp32 RF <= 1e-5 contract
+    ("b200tc" profile only).
     Reference-profile spaces, tables and dispatchers are unchanged.
     """
 
@@ -59,9 +63,10 @@ class KernelFamily(str, Enum):
     TMA = "tma"
     SKINNY_N = "skinny_n"
     SKINNY_M = "skinny_m"
+    TF32X3 = "tf32x3"
 
 
-TC_FAMILIES = (KernelFamily.TF32, KernelFamily.BF16)
+TC_FAMILIES = (KernelFamily.TF32, KernelFamily.BF16, KernelFamily.TF32X3)
 
 
 REFERENCE_FAMILIES = (KernelFamily.DIRECT, KernelFamily.INDIRECT)
@@ -72,7 +77,8 @@ _FAMILY_CODE = {KernelFamily.DIRECT: _native.AG_FAMILY_DIRECT,
                 KernelFamily.BF16: _native.AG_FAMILY_BF16,
                 KernelFamily.TMA: _native.AG_FAMILY_TMA,
                 KernelFamily.SKINNY_N: _native.AG_FAMILY_SKINNY_N,
-                KernelFamily.SKINNY_M: _native.AG_FAMILY_SKINNY_M}
+                KernelFamily.SKINNY_M: _native.AG_FAMILY_SKINNY_M,
+                KernelFamily.TF32X3: _native.AG_FAMILY_TF32X3}
 _CODE_FAMILY = {v: k for k, v in _FAMILY_CODE.items()}
 
 
@@ -138,7 +144,7 @@ class DeviceCaps:
 
     @classmethod
     def b200_tc(cls, **overrides) -> "DeviceCaps":
-        """The B200 profile plus the tensor-core families (tf32, bf16)."""
+        """The B200 profile plus the tensor-core families (tf32, bf16, tf32x3)."""
         kw = dict(spaces.B200_CAPS)
         kw["profile"] = spaces.PROFILE_B200_TC
         kw.update(overrides)
@@ -258,7 +264,8 @@ def enumerate_search_space(family: KernelFamily, caps: DeviceCaps = DeviceCaps()
 
 def full_search_space(caps: DeviceCaps = DeviceCaps()) -> list[KernelConfig]:
     """All families concatenated: direct block first, then indirect (then, in
-    the B200 profiles only, split-K, and in b200tc the tf32/bf16 families)."""
+    the B200 profiles only, split-K, TMA, skinny, and in b200tc the tensor-core
+    families) -- KernelFamily order, so existing class ids keep their meaning."""
     out = []
     for fam in KernelFamily:
         out.extend(enumerate_search_space(fam, caps))

@@ -69,10 +69,14 @@ SPLITK_SLICES = (2, 4, 8, 16)
 # only the b200tc search space: their numerics (tf32 / bf16 inputs, fp32
 # accumulation) differ from the fp32 families, so fp32 tables and trees
 # keep their meaning.
-TC_FAMILIES = ("tf32", "bf16")
+# "tf32x3" (3xTF32, fp32-accurate): the tf32 kernel with [hi | lo] parts of
+# both operands in every stage and three MMAs per K step (twice the stage
+# bytes of tf32).
+TC_FAMILIES = ("tf32", "bf16", "tf32x3")
 TC_BLOCK_M = (128, 256)
 TC_BLOCK_N = (64, 128, 256)
-TC_BLOCK_K = {"tf32": 32, "bf16": 64}
+TC_BLOCK_K = {"tf32": 32, "bf16": 64, "tf32x3": 32}
+TC_PARTS = {"tf32": 1, "bf16": 1, "tf32x3": 2}
 TC_STAGES = (2, 3, 4, 6)
 TC_SMEM_LIMIT = 227 * 1024
 # B200 profiles, TMA family ("tma"): the indirect core's tiles fed by TMA
@@ -111,11 +115,12 @@ def is_b200_profile(profile) -> bool:
 TC_EPILOGUE_BYTES = 4 * 32 * 36 * 4  # per-warp 32 x 32 fp32 staging blocks (tc_kernels.cuh EPI_BYTES)
 
 
-def tc_smem_bytes(bm, bn, stages) -> int:
+def tc_smem_bytes(bm, bn, stages, parts=1) -> int:
     """Dynamic shared memory of one tc CTA: the stage ring (128 rows of A and
-    bn / (bm / 128) rows of B per stage) + slack + epilogue staging + barriers."""
+    bn / (bm / 128) rows of B per stage and operand part) + slack + epilogue
+    staging + barriers."""
     ctas = bm // 128
-    return stages * (128 + bn // ctas) * 128 + 1024 + TC_EPILOGUE_BYTES + 256
+    return stages * parts * (128 + bn // ctas) * 128 + 1024 + TC_EPILOGUE_BYTES + 256
 
 # DeviceCaps defaults (kernels.py:64-71) and the B200 profile caps
 REFERENCE_CAPS = dict(tile_memory_cap=32768, register_tile_cap_direct=8,
@@ -151,7 +156,7 @@ def is_legal_tuple(family, bm, bn, bk, tm, tn, uk, caps) -> bool:
         # a pair splits B into whole 128-byte chunks per CTA (64 bf16 / 32 tf32)
         if bm == 256 and (bn // 2) % (128 // (2 if family == "bf16" else 4)):
             return False
-        return tc_smem_bytes(bm, bn, tm) <= TC_SMEM_LIMIT
+        return tc_smem_bytes(bm, bn, tm, TC_PARTS[family]) <= TC_SMEM_LIMIT
     if family == "direct" and uk != 1:
         return False
     if family == "skinny_n":

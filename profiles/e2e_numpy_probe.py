@@ -2,6 +2,8 @@
 caller's bytes can cross PCIe (measurement only):
   pageable   -- ag_gemm_host_ex, flags 0 (the driver stages each copy)
   register   -- ag_gemm_host_ex, AG_HOST_REGISTER (page-locked for the call)
+  stage      -- ag_gemm_host_ex, AG_HOST_STAGE (pinned rings + host copy workers)
+  stage_fresh -- AG_HOST_STAGE into a freshly allocated output each call (numpy's out=None)
   pinned     -- the operands already in pinned memory (torch pin_memory)
     python profiles/e2e_numpy_probe.py     (on the GPU box)"""
 import ctypes
@@ -33,9 +35,11 @@ def main():
         ns = native_shape(s)
         row = {"mnk": list(s.mnk), "mb": round((A.nbytes + B.nbytes + out.nbytes) / 1e6, 1)}
         secs = ctypes.c_double()
-        for name, flags in (("pageable", 0), ("register", 1)):
+        for name, flags in (("pageable", 0), ("register", 1), ("stage", 2), ("stage_fresh", 2)):
             ts = []
             for _ in range(4):
+                if name == "stage_fresh":
+                    out = np.empty_like(out)
                 t0 = time.perf_counter()
                 rc = lib.ag_gemm_host_ex(ctypes.byref(ns), ctypes.byref(cfg), ctypes.byref(nc), 0, A.ctypes.data,
                                          A.shape[1], B.ctypes.data, B.shape[1], C.ctypes.data, C.shape[1],

@@ -96,3 +96,59 @@ extern "C" double empty_launch(void* flush, size_t flush_bytes, int reps) {
     return best * 1e-3;
 }
 extern "C" void do_flush_ext(void* flush, size_t bytes, int r) { do_flush(flush, bytes, r); }
+
+// ---- streaming-read floor: how long a pure read of `bytes` takes in the
+// bench regime (flush, event, one kernel, event).  Each CTA reads one
+// contiguous chunk with UNROLL independent 16-byte loads in flight per
+// thread.  The floor any skinny GEMM over an operand of that size can reach.
+template <int UNROLL>
+__global__ void __launch_bounds__(256) chunk_read_kernel(const float4* __restrict__ p, size_t n, float* sink) {
+    const size_t per = (n + gridDim.x - 1) / gridDim.x;
+    const size_t b = blockIdx.x * per, e = min(n, b + per);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (size_t i = b + threadIdx.x; i < e; i += 256 * UNROLL) {
+        float4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const size_t j = i + (size_t)u * 256;
+            v[u] = j < e ? __ldg(p + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 1234.5f) *sink = acc.x;
+}
+
+extern "C" double read_floor(const void* src, size_t bytes, int ctas, int unroll, void* flush, size_t flush_bytes,
+                             int reps) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto go = [&]() {
+        const float4* p = (const float4*)src;
+        float* sink = (float*)flush;
+        if (unroll == 4) chunk_read_kernel<4><<<ctas, 256>>>(p, bytes / 16, sink);
+        else if (unroll == 8) chunk_read_kernel<8><<<ctas, 256>>>(p, bytes / 16, sink);
+        else chunk_read_kernel<16><<<ctas, 256>>>(p, bytes / 16, sink);
+    };
+    go();
+    cudaDeviceSynchronize();
+    double s[64];
+    reps = reps > 64 ? 64 : reps;
+    for (int r = 0; r < reps; ++r) {
+        do_flush(flush, flush_bytes, r);
+        cudaEventRecord(e0, 0);
+        go();
+        cudaEventRecord(e1, 0);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        s[r] = ms * 1e-3;
+    }
+    for (int a = 0; a < reps; ++a)
+        for (int b = a + 1; b < reps; ++b)
+            if (s[b] < s[a]) { double t = s[a]; s[a] = s[b]; s[b] = t; }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return s[reps / 2];
+}

@@ -1,4 +1,4 @@
-"""GPU parity of the tensor-core families (tf32, bf16; csrc/tc_kernels.cuh).
+"""GPU parity of the tensor-core families (tf32, bf16, tf32x3; csrc/tc_kernels.cuh).
 
 No reference analogue (BASELINE.json configs[4] adds them to the search
 space).  Bars, as SURVEY.md section 8(c) states them:
@@ -9,6 +9,9 @@ space).  Bars, as SURVEY.md section 8(c) states them:
   them (tf32: the tensor core reads the fp32 bits and drops the low 13
   mantissa bits; bf16: the convert pass rounds to nearest even): <= 1e-5,
   i.e. only fp32 accumulation error remains.
+* tf32x3 (3xTF32: hi/lo operand split, three tf32 MMAs per K step) is held
+  to the fp32 families' bar: <= 1e-5 vs the float64 reference on the
+  float32 inputs themselves, at every K.
 beta == 0 never reads C (the indirect family's semantics, kernels.py:318-321).
 """
 
@@ -23,7 +26,8 @@ from paper_1806_07060_b200.kernels import (DeviceCaps, KernelConfig, KernelFamil
 pytestmark = pytest.mark.gpu
 
 TC = DeviceCaps.b200_tc()
-RF_TOL = {KernelFamily.TF32: 1e-3, KernelFamily.BF16: 1e-2}
+RF_TOL = {KernelFamily.TF32: 1e-3, KernelFamily.BF16: 1e-2, KernelFamily.TF32X3: 1e-5}
+FAMS = [KernelFamily.TF32, KernelFamily.BF16, KernelFamily.TF32X3]
 RF_TOL_ROUNDED = 1e-5
 
 
@@ -46,7 +50,7 @@ def round_bf16(x):
     return r.astype(np.uint32).view(np.float32)
 
 
-ROUND = {KernelFamily.TF32: round_tf32, KernelFamily.BF16: round_bf16}
+ROUND = {KernelFamily.TF32: round_tf32, KernelFamily.BF16: round_bf16, KernelFamily.TF32X3: lambda x: x}
 
 
 def _ref(s, A, B, C):
@@ -73,12 +77,12 @@ def _configs(fam):
 
 
 def test_tc_space_enumerates_only_in_tc_profile():
-    for fam in (KernelFamily.TF32, KernelFamily.BF16):
+    for fam in FAMS:
         assert enumerate_search_space(fam, DeviceCaps.b200()) == []
         assert len(_configs(fam)) >= 6
 
 
-@pytest.mark.parametrize("fam", [KernelFamily.TF32, KernelFamily.BF16], ids=lambda f: f.value)
+@pytest.mark.parametrize("fam", FAMS, ids=lambda f: f.value)
 @pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 13, 5), (128, 128, 32), (129, 257, 33), (35, 1000, 2560),
                                  (300, 64, 1), (64, 300, 4097)])
 @pytest.mark.parametrize("trans", [(False, False), (True, False), (False, True), (True, True)],
@@ -88,7 +92,7 @@ def test_tc_shapes_and_transposes(fam, mnk, trans):
     _check(s, _configs(fam)[0])
 
 
-@pytest.mark.parametrize("fam", [KernelFamily.TF32, KernelFamily.BF16], ids=lambda f: f.value)
+@pytest.mark.parametrize("fam", FAMS, ids=lambda f: f.value)
 def test_tc_every_config(fam):
     # 333 x 517 x 260: ragged in every dimension; the persistent grid wraps
     # when tiles exceed the SM count (checked at 2048^2 below)
@@ -97,7 +101,7 @@ def test_tc_every_config(fam):
         _check(s, cfg)
 
 
-@pytest.mark.parametrize("fam", [KernelFamily.TF32, KernelFamily.BF16], ids=lambda f: f.value)
+@pytest.mark.parametrize("fam", FAMS, ids=lambda f: f.value)
 def test_tc_persistent_wrap_rows(fam):
     """2048 x 2048 x 1024: up to 512 tiles over 148 persistent CTAs.  Checked
     on 64 exact rows spread over the matrix (pre-rounded float64)."""
@@ -111,7 +115,7 @@ def test_tc_persistent_wrap_rows(fam):
         assert rel_frobenius(out[rows], exact) <= RF_TOL_ROUNDED, cfg.canonical()
 
 
-@pytest.mark.parametrize("fam", [KernelFamily.TF32, KernelFamily.BF16], ids=lambda f: f.value)
+@pytest.mark.parametrize("fam", FAMS, ids=lambda f: f.value)
 def test_tc_beta_zero_never_reads_c(fam):
     s = ProblemShape(70, 90, 40, alpha=2.0, beta=0.0)
     A, B, C = rand_operands(s, np.float32, 5)
@@ -129,3 +133,18 @@ def test_tc_rejects_float64():
     A, B, C = rand_operands(s, np.float64)
     with pytest.raises(ConfigError):
         gemm_execute(s, _configs(KernelFamily.TF32)[0], A, B, C, TC)
+
+
+@pytest.mark.parametrize("mnk", [(256, 256, 8192), (1000, 700, 4096), (35, 2000, 2560)])
+def test_tf32x3_accuracy_matches_fp32_families(mnk):
+    """3xTF32 against the CUDA-core fp32 path on the same inputs: both within
+    the fp32 bar of the float64 product, and the tensor-pipe error no more
+    than 4x the FFMA error (long K included)."""
+    s = ProblemShape(*mnk)
+    A, B, C = rand_operands(s, np.float32, 11)
+    ref = _ref(s, A, B, C)
+    x3, _ = gemm_execute(s, _configs(KernelFamily.TF32X3)[-1], A, B, C, TC)
+    f32, _ = gemm_execute(s, KernelConfig(KernelFamily.INDIRECT, 64, 64, 16, 4, 4, 1), A, B, C, TC)
+    e3, e32 = rel_frobenius(x3, ref), rel_frobenius(f32, ref)
+    assert e3 <= 1e-5 and e32 <= 1e-5, (e3, e32)
+    assert e3 <= 4 * e32 + 1e-7, (e3, e32)
