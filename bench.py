@@ -46,6 +46,10 @@ PO2_BUNDLE = DATA / "tables_b200_po2.csv.gz"
 DB_BUNDLE = DATA / "tables_b200_deepbench.csv.gz"
 TC_BUNDLE = DATA / "tables_b200tc_random.csv.gz"
 GO2_BUNDLE = DATA / "tables_b200_go2.csv.gz"
+# the fp32 space plus the fp32-accurate tensor-pipe family tf32x3 (same
+# sweeps, tf32x3 rows merged in: configs/*_x3.json)
+X3_PO2_BUNDLE = DATA / "tables_b200x3_po2.csv.gz"
+X3_DB_BUNDLE = DATA / "tables_b200x3_deepbench.csv.gz"
 TRAFFIC_FILE = ROOT / "profiles" / "roofline_traffic.json"
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -294,6 +298,8 @@ def pack_launches(shape, cfg) -> int:
             and shape.K % 4 == 0 and (cfg.family is KernelFamily.SKINNY_M or shape.N % 4 == 0):
         return 1  # one clustered launch (skinny.cuh)
     if cfg.family in TC_FAMILIES:  # bf16: one convert pass per operand; tf32 reads fp32 in place
+        if cfg.family is KernelFamily.TF32X3:
+            return 2  # one convert launch (both lo parts) + the tc kernel
         return 3 if cfg.family is KernelFamily.BF16 else 1
     if cfg.family is KernelFamily.TMA and not shape.transA and not shape.transB and shape.K % 4 == 0 \
             and shape.N % 4 == 0:
@@ -614,6 +620,10 @@ def run_ours(args):
     except Exception as exc:  # noqa: BLE001
         tc_doc = {"error": f"{type(exc).__name__}: {exc}"}
     try:
+        x3_doc = x3_section(cases, default_t, device, distributed, times, fallback, args)
+    except Exception as exc:  # noqa: BLE001
+        x3_doc = {"error": f"{type(exc).__name__}: {exc}"}
+    try:
         go2_doc = go2_section() if rank == 0 else None
     except Exception as exc:  # noqa: BLE001
         go2_doc = {"error": f"{type(exc).__name__}: {exc}"}
@@ -733,9 +743,10 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h,
                 "how": "codegen.dispatch_and_run(tree, shape, A, B, C, caps, classes) on plain pageable numpy "
                        "arrays (the reference's call, codegen.py:285-325): cached compiled selector, then the "
-                       "compiled numpy path (csrc/fastpath.c) -> ag_gemm_host_ex: host buffers page-locked for "
-                       "the call, H2D / family path / D2H pipelined over output panels on three streams; median "
-                       "of 3 wall-clock calls per shape",
+                       "compiled numpy path (csrc/fastpath.c) -> ag_gemm_host_ex(AG_HOST_STAGE): the pageable "
+                       "operands and the fresh output cross through pinned staging rings filled / drained by "
+                       "parallel host copies, H2D / family path / D2H pipelined over output panels on three "
+                       "streams; median of 3 wall-clock calls per shape",
                 "pinned_dispatch_native": round(e2e_pinned * world, 2)},
         "roofline": {"bound": "fp32-cuda-core (compute)", "achieved": round(achieved, 3),
                      "peak": round(peak_meas, 3), "unit": "TFLOP/s", "frac": round(achieved / peak_meas, 4),
@@ -746,6 +757,7 @@ def run_ours(args):
                      "note": "event time covers the whole family path (pack helpers + tiled core)"},
         "cpu_baseline": cpu,
         "tc_random": tc_doc,
+        "fp32_accurate_tc": x3_doc,
         "go2_table_mode": go2_doc,
         "sweep": sweep_doc,
         "clocks": clocks,
@@ -822,6 +834,73 @@ def tc_section(m, policy, device, distributed, times, fallback, args):
             "fixed_tc_geomean": round(g_fx, 1), "fixed_tc_config": tcm["fixed_tc"].canonical(),
             "dt_over_oracle": round(g_dt / g_or, 4), "dt_over_default": round(g_dt / g_de, 4),
             "dt_over_fixed_tc": round(g_dt / g_fx, 4), "dt_families": fams, "roofline": roof,
+            "per_shape": [[list(c.shape.mnk), round(a, 1), round(b, 1), d.canonical(), o.canonical()]
+                          for c, a, b, d, o in zip(cases, rate(dt_t), rate(or_t), dt_cfgs, or_cfgs)]}
+
+
+def x3_section(cases, default_t, device, distributed, times, fallback, args):
+    """The fp32 space plus tf32x3 (fp32-accurate 3xTF32 on tcgen05, RF <=
+    1e-5 like the fp32 families): the reference pipeline on the merged po2
+    tables (no DeepBench shape in training), the DT measured live on the
+    DeepBench set against the merged oracle and the fp32 default tile; the
+    whole output of the largest tf32x3 pick checked against the float64
+    product; roofline of the dominant tf32x3 kernel against tf32 peak / 3."""
+    import torch
+
+    from paper_1806_07060_b200 import codegen
+    from paper_1806_07060_b200.kernels import DeviceCaps, KernelFamily
+    from paper_1806_07060_b200.tuner import load_table_bundle
+
+    if not X3_PO2_BUNDLE.exists() or not X3_DB_BUNDLE.exists():
+        return {"unavailable": f"no {X3_PO2_BUNDLE.name} / {X3_DB_BUNDLE.name}"}
+    po2 = load_table_bundle(X3_PO2_BUNDLE)
+    db = {t.shape.mnk: t for t in load_table_bundle(X3_DB_BUNDLE)}
+    pipe = _pipeline(po2, "po2")
+    sel = codegen.CompiledSelector(pipe["tree"], pipe["classes"])
+    runner = Runner(device, DeviceCaps.b200_tc())
+    reps = max(4, args.steps // 2)
+
+    def timed(how):
+        runner.pass_(cases, how)
+        runs = [times(runner.pass_(cases, how)) for _ in range(reps)]
+        return distributed.reduce_max([trimmed_mean([r[i] for r in runs]) for i in range(len(cases))], device)
+
+    dt_t = timed(lambda i, c: runner.launch(c, selector=sel, fallback=fallback))
+    dt_cfgs = [sel.select(*c.shape.mnk) for c in cases]
+    or_cfgs = [db[c.shape.mnk].best_config for c in cases]
+    nat = [c.native() for c in or_cfgs]
+    or_t = timed(lambda i, c: runner.launch(c, config=nat[i]))
+    rate = lambda ts: [c.flops / t / 1e9 for c, t in zip(cases, ts)]  # noqa: E731
+    g_dt, g_or, g_de = geomean(rate(dt_t)), geomean(rate(or_t)), geomean(rate(default_t))
+    x3_idx = [i for i, c in enumerate(dt_cfgs) if c.family is KernelFamily.TF32X3]
+    roof, parity = None, None
+    if x3_idx:
+        dom = max(x3_idx, key=lambda i: dt_t[i])
+        c = cases[dom]
+        runner.launch(c, config=dt_cfgs[dom].native())
+        torch.cuda.synchronize()
+        exact = c.dA.double() @ c.dB.double()
+        parity = {"shape": list(c.shape.mnk), "config": dt_cfgs[dom].canonical(),
+                  "rf_whole_matrix": float(torch.linalg.norm(c.dout.double() - exact) / torch.linalg.norm(exact)),
+                  "bar": 1e-5}
+        del exact
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        tf32_peak = float(peaks.get("bf16_tflops", 2250.0)) / 2
+        ach = c.flops / dt_t[dom] / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32_peak / 3, 1), "unit": "TFLOP/s",
+                "frac": round(ach / (tf32_peak / 3), 4), "kernel": f"{'x'.join(map(str, c.shape.mnk))}:"
+                                                                  f"{dt_cfgs[dom].canonical()}",
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 2 = tf32, / 3 products per K step",
+                "note": "event time covers the family path (lo-part convert pass included)"}
+    fams = {}
+    for c in dt_cfgs:
+        fams[c.family.value] = fams.get(c.family.value, 0) + 1
+    return {"workload": "deepbench_fp32 (same 40 shapes, same regime as the headline)",
+            "space": "b200 fp32 families + tf32x3 (fp32-accurate, RF <= 1e-5)",
+            "model": pipe["name"], "n_train": pipe["n_train"], "score_table_mode": pipe["score"],
+            "dt_geomean": round(g_dt, 1), "oracle_geomean": round(g_or, 1), "default_geomean": round(g_de, 1),
+            "dt_over_oracle": round(g_dt / g_or, 4), "dt_over_default": round(g_dt / g_de, 4),
+            "dt_families": fams, "roofline": roof, "parity": parity,
             "per_shape": [[list(c.shape.mnk), round(a, 1), round(b, 1), d.canonical(), o.canonical()]
                           for c, a, b, d, o in zip(cases, rate(dt_t), rate(or_t), dt_cfgs, or_cfgs)]}
 
