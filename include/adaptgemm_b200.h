@@ -161,7 +161,7 @@ int ag_gemm_host(const ag_shape* shape, const ag_config* config, const ag_caps* 
  * the reference's `seconds` without the copies. */
 #define AG_HOST_REGISTER 1
 /* flags & AG_HOST_STAGE: pageable host buffers cross through two
- * library-owned pinned rings (4 x 16 MB each per thread and device): a pool
+ * library-owned pinned rings (8 x 4 MB each per thread and device): a pool
  * of host copy workers fills / drains ring slots while the copy engines move
  * the neighbouring slots and the kernels run.  Pinned buffers are DMA'd
  * directly.  Takes precedence over AG_HOST_REGISTER for pageable buffers. */

@@ -511,6 +511,7 @@ int ag_is_legal(const ag_config* c, const ag_caps* caps) {
         const int parts = c->family == AG_FAMILY_TF32X3 ? 2 : 1;
         if ((c->bm != 128 && c->bm != 256) || c->bk != bk || c->tn != 1 || c->uk != 1) return 0;
         if (c->bn % 32 || c->bn < 32 || c->bn > 256 || c->tm < 2 || c->tm > 8) return 0;
+        if (parts == 2 && c->bn > 128) return 0;  // tf32x3: bn-wide fp32 running sum per epilogue thread
         const int ctas = c->bm / 128;
         if (ctas == 2 && (c->bn / 2) % chunk) return 0;
         const int64_t smem =

@@ -52,7 +52,8 @@ constexpr int KIND_TF32X3 = 2;  // fp32-accurate: 3 tf32 products over hi / lo o
 constexpr int BM = 128;          // UMMA M (cta_group::1): TMEM lane = output row
 constexpr int ROW_BYTES = 128;   // one K block = one 128-byte swizzle row
 constexpr int THREADS = 192;     // producer warp, MMA warp, 4 epilogue warps
-constexpr int ACC_STAGES = 2;    // TMEM accumulator double buffer
+constexpr int ACC_STAGES_MAX = 2;  // TMEM accumulator double buffer (when 2 buffers fit 512 columns)
+constexpr int X3_CHUNK_BLOCKS = 8;  // 3xTF32: K blocks (8 x 32 = 256 k) per TMEM accumulation chunk
 
 inline constexpr i64 round_up_i(i64 x, i64 s) { return (x + s - 1) / s * s; }
 
@@ -198,10 +199,16 @@ __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& tm, i
     tn = r / gs;
 }
 
-template <int BN>
+// one accumulator buffer = ACC_PARTS x BN fp32 columns (3xTF32 keeps its two
+// small products in a second accumulator); double buffered when two fit
+template <int BN, int ACC_PARTS>
+constexpr int acc_stages() {
+    return 2 * ACC_PARTS * BN <= 512 ? ACC_STAGES_MAX : 1;
+}
+template <int BN, int ACC_PARTS = 1>
 constexpr uint32_t tmem_cols() {
-    return (ACC_STAGES * BN) <= 32 ? 32 : (ACC_STAGES * BN) <= 64 ? 64 : (ACC_STAGES * BN) <= 128 ? 128
-                                     : (ACC_STAGES * BN) <= 256 ? 256 : 512;
+    constexpr int c = acc_stages<BN, ACC_PARTS>() * ACC_PARTS * BN;
+    return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
 }
 
 // per-CTA shared memory: the stage ring (A: 128 rows, B: BN / CTAS rows of
@@ -279,7 +286,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     constexpr int BNC = BN / CTAS;  // B rows (N) staged by each CTA
     constexpr uint32_t A_BYTES = BM * ROW_BYTES, B_BYTES = BNC * ROW_BYTES;  // one part
     constexpr uint32_t STAGE_TX = (A_BYTES + B_BYTES) * CTAS * PARTS;
-    constexpr uint32_t TMEM_COLS = tmem_cols<BN>();
+    // The tensor core's fp32 accumulation is not round-to-nearest: with exact
+    // products (tf32-truncated inputs) its error grows linearly in K (RF
+    // 6.0e-6 at K = 2560, 1.9e-5 at 8192, 7.7e-5 at 32768, against 0.9e-6 /
+    // 1.6e-6 / 3.2e-6 for FFMA; profiles/r02_tc_accuracy.jsonl).  3xTF32
+    // therefore accumulates in TMEM over chunks of KC K blocks only: each
+    // chunk's accumulator is drained by the epilogue warps and added in IEEE
+    // fp32 to a per-thread running sum (one output row per thread, BN <= 128
+    // registers), while the MMA issuer fills the other TMEM buffer.
+    constexpr int KC = PARTS == 2 ? X3_CHUNK_BLOCKS : 0;  // 0: the whole K range in TMEM
+    static_assert(KC == 0 || BN <= 128, "3xTF32 keeps a BN-wide fp32 running sum per epilogue thread");
+    constexpr int ACC_STAGES = acc_stages<BN, 1>();
+    constexpr uint32_t ACC_COLS = (uint32_t)BN;
+    constexpr uint32_t TMEM_COLS = tmem_cols<BN, 1>();
     constexpr int K_STEPS = BK / Elem<KIND>::UMMA_K;
     constexpr int CH = ROW_BYTES / (int)sizeof(typename Elem<KIND>::T);  // elements per 128-byte MN chunk
     constexpr uint32_t CHUNK_BYTES = BK * ROW_BYTES;                      // one MN chunk of one stage
@@ -419,10 +438,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int t = unit; t < tiles; t += units) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+                uint32_t d = 0;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    const int kc = KC ? kb % KC : kb;  // K block within the accumulation chunk
+                    if (kc == 0) {  // a new chunk: publish the last one, take a free accumulator
+                        if (kb > 0) {
+                            if constexpr (CTAS == 1) {
+                                umma_commit(&tfull[acc]);
+                            } else {
+                                umma_commit_pair(&tfull[acc]);
+                            }
+                            if (++acc == ACC_STAGES) {
+                                acc = 0;
+                                acc_phase ^= 1;
+                            }
+                        }
+                        mbar_wait(&tempty[acc], acc_phase ^ 1);
+                        tc_fence_after();
+                        d = tmem_base + (uint32_t)acc * ACC_COLS;
+                    }
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a0 = smem_addr(sA + stage * PARTS * A_BYTES);
@@ -447,12 +481,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
 #pragma unroll
                     for (int k = 0; k < K_STEPS; ++k) {
                         const uint64_t ad = adesc(a0, k), bd = bdesc(b0, k);
+                        const uint32_t acc_on = (kc | k) != 0;
                         if constexpr (PARTS == 2) {  // small products first: a_lo.b_hi, a_hi.b_lo, a_hi.b_hi
-                            mma(adesc(a0 + A_BYTES, k), bd, (kb | k) != 0);
+                            mma(adesc(a0 + A_BYTES, k), bd, acc_on);
                             mma(ad, bdesc(b0 + B_BYTES, k), 1u);
                             mma(ad, bd, 1u);
                         } else {
-                            mma(ad, bd, (kb | k) != 0);
+                            mma(ad, bd, acc_on);
                         }
                     }
                     if constexpr (CTAS == 1) {
@@ -485,16 +520,58 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         float* blk = sEpi + q * 32 * EPI_LD;
         int acc = 0;
         uint32_t acc_phase = 0;
+        // release the TMEM buffer `acc` to the MMA issuer (every CTA's epilogue warps)
+        auto release = [&]() {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0) {
+                    mbar_arrive(&tempty[acc]);
+                } else {
+                    mbar_arrive_remote(&tempty[acc], 0);
+                }
+            }
+            if (++acc == ACC_STAGES) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        };
+        const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
         for (int t = unit; t < tiles; t += units) {
             int tm, tn;
             tile_coords(p, t, tm, tn);
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
             const int row0 = tm * BM * CTAS + (int)rank * BM + q * 32;  // first row of this warp's block
-#pragma unroll 1
+            // 3xTF32: IEEE fp32 running sum of the chunk accumulators (this thread's row)
+            float run[KC ? BN : 1];
+            if constexpr (KC != 0) {
+#pragma unroll
+                for (int j = 0; j < BN; ++j) run[j] = 0.f;
+                const int chunks = (p.k_blocks + KC - 1) / KC;
+                for (int ch = 0; ch < chunks; ++ch) {
+                    mbar_wait(&tfull[acc], acc_phase);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c0 = 0; c0 < BN; c0 += 32) {
+                        uint32_t v[32];
+                        tmem_ld32(lane_base + (uint32_t)acc * ACC_COLS + (uint32_t)c0, v);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) run[c0 + j] += __uint_as_float(v[j]);
+                    }
+                    release();
+                }
+            } else {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+            }
+#pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t v[32];
-                tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+                if constexpr (KC != 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(run[c0 + j]);
+                } else {
+                    tmem_ld32(lane_base + (uint32_t)acc * ACC_COLS + (uint32_t)c0, v);
+                }
                 const int col0 = tn * BN + c0;
                 if (row0 >= p.M || col0 >= p.N) continue;  // warp-uniform
 #pragma unroll
@@ -538,19 +615,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 }
                 __syncwarp();
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (rank == 0) {
-                    mbar_arrive(&tempty[acc]);
-                } else {
-                    mbar_arrive_remote(&tempty[acc], 0);
-                }
-            }
-            if (++acc == ACC_STAGES) {
-                acc = 0;
-                acc_phase ^= 1;
-            }
+            if constexpr (KC == 0) release();
         }
     }
     tc_fence_before();

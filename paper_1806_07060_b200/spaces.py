@@ -71,7 +71,8 @@ SPLITK_SLICES = (2, 4, 8, 16)
 # keep their meaning.
 # "tf32x3" (3xTF32, fp32-accurate): the tf32 kernel with [hi | lo] parts of
 # both operands in every stage and three MMAs per K step (twice the stage
-# bytes of tf32).
+# bytes of tf32); TMEM accumulates 256-k chunks that the epilogue sums in
+# IEEE fp32, so bn <= 128.
 TC_FAMILIES = ("tf32", "bf16", "tf32x3")
 TC_BLOCK_M = (128, 256)
 TC_BLOCK_N = (64, 128, 256)
@@ -155,6 +156,9 @@ def is_legal_tuple(family, bm, bn, bk, tm, tn, uk, caps) -> bool:
             return False
         # a pair splits B into whole 128-byte chunks per CTA (64 bf16 / 32 tf32)
         if bm == 256 and (bn // 2) % (128 // (2 if family == "bf16" else 4)):
+            return False
+        # tf32x3 keeps a bn-wide fp32 running sum per epilogue thread (tc_kernels.cuh)
+        if family == "tf32x3" and bn > 128:
             return False
         return tc_smem_bytes(bm, bn, tm, TC_PARTS[family]) <= TC_SMEM_LIMIT
     if family == "direct" and uk != 1:

@@ -13,7 +13,7 @@ import pytest
 
 from conftest import ROOT
 from paper_1806_07060_b200 import _native, spaces
-from paper_1806_07060_b200.kernels import (
+from paper_1806_07060_b200.kernels import (TC_FAMILIES,
     DeviceCaps,
     KernelConfig,
     KernelFamily,
@@ -92,7 +92,7 @@ def test_workspace_sizes():
 def test_native_tc_legality_equals_python():
     lib = _native.lib()
     ncaps = DeviceCaps.b200_tc().native()
-    for fam in (KernelFamily.TF32, KernelFamily.BF16):
+    for fam in (KernelFamily.TF32, KernelFamily.BF16, KernelFamily.TF32X3):
         for bm in (64, 128, 256):
             for bn in (16, 32, 64, 96, 128, 192, 256, 288):
                 for bk in (16, 32, 64):
@@ -105,8 +105,9 @@ def test_native_tc_legality_equals_python():
 
 def test_tc_space_has_kernels_float32_only():
     lib = _native.lib()
-    tc = [c for c in full_search_space(DeviceCaps.b200_tc()) if c.family in (KernelFamily.TF32, KernelFamily.BF16)]
-    assert len(tc) >= 30
+    tc = [c for c in full_search_space(DeviceCaps.b200_tc()) if c.family in TC_FAMILIES]
+    assert len(tc) >= 44
+    assert {c.family for c in tc} == set(TC_FAMILIES)
     assert {c.block_m for c in tc} == {128, 256}  # one CTA and CTA-pair (cta_group::2) tiles
     for cfg in tc:
         assert lib.ag_has_kernel(ctypes.byref(cfg.native()), _native.AG_F32), cfg
@@ -120,6 +121,21 @@ def test_tc_workspace_sizes():
     # each 1 KiB rounded
     want = -(-33 * 64 * 2 // 1024) * 1024 + -(-17 * 128 * 2 // 1024) * 1024
     assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(cfg.native()), 0) == want
+    # tf32x3: [A hi | B hi | A lo | B lo], fp32 rows rounded to 32 elements, each part 1 KiB rounded
+    x3 = KernelConfig(KernelFamily.TF32X3, 128, 128, 32, 2, 1, 1)
+    want3 = 2 * (-(-33 * 32 * 4 // 1024) * 1024 + -(-17 * 96 * 4 // 1024) * 1024)
+    assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(x3.native()), 0) == want3
+
+
+def test_tf32x3_split_is_exact():
+    """hi keeps the bits a tf32 MMA reads, lo = x - hi is exact in fp32 and
+    below 2^-10 |x| (the 3xTF32 error budget, tc_kernels.cuh)."""
+    import numpy as np
+    x = np.random.default_rng(0).uniform(-1e3, 1e3, 100000).astype(np.float32)
+    hi = (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    lo = x - hi
+    assert np.array_equal(hi.astype(np.float64) + lo.astype(np.float64), x.astype(np.float64))
+    assert np.all(np.abs(lo) <= np.abs(x) * 2.0 ** -10)
 
 
 def test_host_scratch_bytes():
