@@ -46,10 +46,10 @@ PO2_BUNDLE = DATA / "tables_b200_po2.csv.gz"
 DB_BUNDLE = DATA / "tables_b200_deepbench.csv.gz"
 TC_BUNDLE = DATA / "tables_b200tc_random.csv.gz"
 GO2_BUNDLE = DATA / "tables_b200_go2.csv.gz"
-# the fp32 space plus the fp32-accurate tensor-pipe family tf32x3 (same
-# sweeps, tf32x3 rows merged in: configs/*_x3.json)
-X3_PO2_BUNDLE = DATA / "tables_b200x3_po2.csv.gz"
-X3_DB_BUNDLE = DATA / "tables_b200x3_deepbench.csv.gz"
+# the tf32x3 rows of the same shapes and timing regime (configs/*_x3.json),
+# merged per shape into the fp32 tables by x3_section
+X3_PO2_BUNDLE = DATA / "tables_x3_po2.csv.gz"
+X3_DB_BUNDLE = DATA / "tables_x3_deepbench.csv.gz"
 TRAFFIC_FILE = ROOT / "profiles" / "roofline_traffic.json"
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -838,6 +838,18 @@ def tc_section(m, policy, device, distributed, times, fallback, args):
                           for c, a, b, d, o in zip(cases, rate(dt_t), rate(or_t), dt_cfgs, or_cfgs)]}
 
 
+def load_x3_tables():
+    """(po2, DeepBench) tables of the fp32 space with the tf32x3 rows of the
+    same shapes merged in (tuner.merge_tables: fp32 rows first)."""
+    from paper_1806_07060_b200.tuner import load_table_bundle, merge_tables
+
+    def merged(base, extra):
+        by = {t.shape.mnk: t for t in load_table_bundle(extra)}
+        return [merge_tables(t, by[t.shape.mnk]) for t in load_table_bundle(base)]
+
+    return merged(PO2_BUNDLE, X3_PO2_BUNDLE), merged(DB_BUNDLE, X3_DB_BUNDLE)
+
+
 def x3_section(cases, default_t, device, distributed, times, fallback, args):
     """The fp32 space plus tf32x3 (fp32-accurate 3xTF32 on tcgen05, RF <=
     1e-5 like the fp32 families): the reference pipeline on the merged po2
@@ -849,12 +861,10 @@ def x3_section(cases, default_t, device, distributed, times, fallback, args):
 
     from paper_1806_07060_b200 import codegen
     from paper_1806_07060_b200.kernels import DeviceCaps, KernelFamily
-    from paper_1806_07060_b200.tuner import load_table_bundle
-
     if not X3_PO2_BUNDLE.exists() or not X3_DB_BUNDLE.exists():
         return {"unavailable": f"no {X3_PO2_BUNDLE.name} / {X3_DB_BUNDLE.name}"}
-    po2 = load_table_bundle(X3_PO2_BUNDLE)
-    db = {t.shape.mnk: t for t in load_table_bundle(X3_DB_BUNDLE)}
+    po2, db_list = load_x3_tables()
+    db = {t.shape.mnk: t for t in db_list}
     pipe = _pipeline(po2, "po2")
     sel = codegen.CompiledSelector(pipe["tree"], pipe["classes"])
     runner = Runner(device, DeviceCaps.b200_tc())

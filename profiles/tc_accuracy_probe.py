@@ -23,7 +23,7 @@ def main():
     rng = np.random.default_rng(0)
     fp32 = KernelConfig.from_canonical("indirect:64-64-16-4-4-1")
     tf32 = KernelConfig.from_canonical("tf32:128-128-32-4-1-1")
-    x3s = [KernelConfig.from_canonical(c) for c in ("tf32x3:128-64-32-4-1-1", "tf32x3:256-256-32-3-1-1")]
+    x3s = [KernelConfig.from_canonical(c) for c in ("tf32x3:128-128-32-3-1-1", "tf32x3:256-128-32-3-1-1")]
 
     def trunc(x):
         return (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
