@@ -61,7 +61,7 @@ class _Caps(ctypes.Structure):
 
 
 # include/adaptgemm_b200.h AG_FAMILY_*; the reference has the first two
-_FAMILY = {"direct": 0, "indirect": 1, "splitk": 2, "tf32": 3, "bf16": 4, "tma": 5, "skinny_n": 6, "skinny_m": 7}
+_FAMILY = {"direct": 0, "indirect": 1, "splitk": 2, "tf32": 3, "bf16": 4, "tma": 5, "skinny_n": 6, "skinny_m": 7, "tf32x3": 8}
 AG_HOST_STAGE = 2
 _P, _I = ctypes.c_void_p, ctypes.c_int64
 _lib = None
