@@ -197,10 +197,12 @@ def build_tc_model(policy):
 
 def go2_section():
     """The paper's dense dataset (go2: 256..3840 step 256, 3375 shapes) on
-    B200 tables (configs/go2_b200.json: the 133-config fp32 shortlist), run
-    through the reference pipeline in table mode: seeded 80/20 split, the
-    5 x 8 CART grid, selection by test DTPR; reports the reference's metrics
-    (accuracy, DTPR, DTTR) and the table-mode geomeans (no GPU time)."""
+    B200 tables swept with the reference's seeded tune_random sampler
+    (configs/go2r_b200.json: 96 of the 1114 B200 configs, tuner.py:188-221,
+    bench regime), run through the reference pipeline in table mode: seeded
+    80/20 split, the 5 x 8 CART grid, selection by test DTPR; reports the
+    reference's metrics (accuracy, DTPR, DTTR) and the table-mode geomeans
+    (no GPU time)."""
     from paper_1806_07060_b200 import evaluation, model
     from paper_1806_07060_b200.dataset import dataset_from_tables, split
     from paper_1806_07060_b200.tuner import load_table_bundle
@@ -230,7 +232,10 @@ def go2_section():
         dt.append(t.gflops_for(cfg))
         orc.append(t.peak_gflops)
         de.append(t.gflops_for(policy.select_config(ProblemShapeOf(mnk))))
-    return {"shapes": len(tables), "configs_per_shape": len(tables[0].measurements), "n_train": len(train_recs),
+    meta = tables[0].meta
+    return {"shapes": len(tables), "configs_per_shape": len(tables[0].measurements),
+            "sampling": {k: meta.get(k) for k in ("mode", "samples", "seed", "l2") if k in meta},
+            "n_train": len(train_recs),
             "n_test": len(test_recs), "model": best.name,
             "accuracy": round(best.accuracy, 4), "dtpr": round(best.dtpr, 4), "dttr": round(best.dttr, 4),
             "leaves": best.stats.total_leaves, "height": best.stats.height,

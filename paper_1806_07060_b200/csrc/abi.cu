@@ -10,7 +10,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -736,13 +738,16 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
             ok(ag::hoststage::h2d(t_pipe.rin, {static_cast<char*>(const_cast<void*>(hsrc)), hp, d, dp, width, rows}, in));
         }
     };
-    auto get = [&](bool pinned, void* hdst, int64_t hp, char* d, int64_t dp, int64_t width, int64_t rows) {
-        if (pinned) {
-            ok(copy2d(hdst, hp, d, dp, width, rows, D2H, back));
-        } else {
-            ok(ag::hoststage::d2h(t_pipe.rout, {static_cast<char*>(hdst), hp, d, dp, width, rows}, back));
-        }
+    // (a staged `get` blocks until the bytes are in the caller's buffer)
+    auto get = [&](bool pinned, void* hdst, int64_t hp, char* d, int64_t dp, int64_t width, int64_t rows,
+                   cudaError_t& err) {
+        const cudaError_t x =
+            pinned ? copy2d(hdst, hp, d, dp, width, rows, D2H, back)
+                   : ag::hoststage::d2h(t_pipe.rout, {static_cast<char*>(hdst), hp, d, dp, width, rows}, back);
+        if (x != cudaSuccess && err == cudaSuccess) err = x;
     };
+    // every event the panels use exists before a second thread looks them up
+    if (!t_pipe.event(2 * (size_t)h.panels + 2)) return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
     // the caller's stream may still be writing the host buffers' producers
     cudaEvent_t start = t_pipe.event(0);
     if (!start) return set_err(AG_ERR_CUDA, "cudaEventCreate failed");
@@ -755,14 +760,47 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
         put(pin_a, dA, h.ca * e, A, lda * e, h.ca * e, h.ra);
     }
     // panel p's output back to the host (after its family path)
-    auto drain = [&](int p) {
+    auto drain = [&](int p, cudaError_t& err) {
         const int64_t x0 = (int64_t)p * h.chunk, w = std::min(h.chunk, h.extent - x0);
-        ok(cudaStreamWaitEvent(back, t_pipe.event(2 + 2 * p), 0));
+        const cudaError_t x = cudaStreamWaitEvent(back, t_pipe.event(2 + 2 * p), 0);
+        if (x != cudaSuccess && err == cudaSuccess) err = x;
         if (h.by_rows) {
-            get(pin_o, static_cast<char*>(out) + x0 * ldo * e, ldo * e, dO + x0 * N * e, N * e, N * e, w);
+            get(pin_o, static_cast<char*>(out) + x0 * ldo * e, ldo * e, dO + x0 * N * e, N * e, N * e, w, err);
         } else {
-            get(pin_o, static_cast<char*>(out) + x0 * e, ldo * e, dO + x0 * e, N * e, w * e, M);
+            get(pin_o, static_cast<char*>(out) + x0 * e, ldo * e, dO + x0 * e, N * e, w * e, M, err);
         }
+    };
+    // A staged (pageable) output drains on its own host thread: the main
+    // thread keeps filling the input ring for the next panels while this one
+    // waits for a panel's kernels and D2H and copies the result out.
+    std::mutex dm;
+    std::condition_variable dcv;
+    int launched = 0;  // panels whose family path is enqueued (-1: abort)
+    cudaError_t drain_err = cudaSuccess;
+    std::thread drainer;
+    const bool drain_thread = !pin_o && h.panels > 1;
+    if (drain_thread) {
+        int dev_id = 0;
+        cudaGetDevice(&dev_id);
+        drainer = std::thread([&, dev_id] {
+            cudaSetDevice(dev_id);  // the current device is per host thread
+            for (int p = 0; p < h.panels; ++p) {
+                {
+                    std::unique_lock<std::mutex> lk(dm);
+                    dcv.wait(lk, [&] { return launched > p || launched < 0; });
+                    if (launched < 0) return;
+                }
+                drain(p, drain_err);
+            }
+        });
+    }
+    auto publish = [&](int n) {
+        if (!drain_thread) return;
+        {
+            std::lock_guard<std::mutex> lk(dm);
+            launched = n;
+        }
+        dcv.notify_one();
     };
     for (int p = 0; p < h.panels; ++p) {
         const int64_t x0 = (int64_t)p * h.chunk, w = std::min(h.chunk, h.extent - x0);
@@ -811,16 +849,26 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
         r = fn(make_call(&ps, c, dtype, pa, pla, pb, plb, pc, N, po, N, dW, h.wsz, run));
         if (k1) ok(cudaEventRecord(k1, run));
         if (r) {
+            publish(-1);
+            if (drainer.joinable()) drainer.join();
             cudaStreamSynchronize(in);
             cudaStreamSynchronize(run);
             cudaStreamSynchronize(back);
             return r;
         }
         ok(cudaEventRecord(edone, run));
-        // the previous panel's output drains while this panel computes
-        if (p >= 1) drain(p - 1);
+        if (drain_thread) {
+            publish(p + 1);
+        } else if (p >= 1) {
+            drain(p - 1, ce);  // the previous panel's output drains while this panel computes
+        }
     }
-    drain(h.panels - 1);
+    if (drain_thread) {
+        drainer.join();
+        ok(drain_err);
+    } else {
+        drain(h.panels - 1, ce);
+    }
     ok(cudaStreamSynchronize(back));
     ok(cudaStreamSynchronize(run));
     ok(cudaStreamSynchronize(in));
