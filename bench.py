@@ -160,8 +160,8 @@ def build_hybrid_model():
 
 def build_tc_model(policy):
     """configs[4]: the reference pipeline on the b200tc tables (random
-    (M, N, K) in 1..8192, tf32/bf16 families + the fp32 winner shortlist;
-    configs/random_tc_b200.json).  Default tile = the fp32 BaselinePolicy of
+    (M, N, K) in 1..8192, tf32/bf16/tf32x3 families + the fp32 winner
+    shortlist, bench regime; configs/random_tc_r02.json).  Default tile = the fp32 BaselinePolicy of
     the main model (the reference's definition); `fixed_tc` = the single tc
     config with the best geomean over the training shapes."""
     from paper_1806_07060_b200 import evaluation, model
