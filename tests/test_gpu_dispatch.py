@@ -344,3 +344,32 @@ def test_dispatch_and_run_numpy_overhead(capsys):
               f"{t_exec * 1e6:.1f} us (+{(t_exec - t_native) * 1e6:.1f}), dispatch_and_run {t_disp * 1e6:.1f} us "
               f"(+{(t_disp - t_native) * 1e6:.1f})")
     assert t_exec - t_native < 20e-6
+
+
+@pytest.mark.parametrize("mnk,name", [((3000, 700, 2048), "indirect:64-128-32-8-8-2"),   # row panels (8)
+                                      ((700, 3000, 2048), "indirect:64-128-32-8-8-2"),   # column panels
+                                      ((4096, 16, 4096), "skinny_n:64-16-32-2-4-4"),     # one big operand
+                                      ((35, 8457, 2560), "skinny_m:40-256-32-1-2-16")])  # N % 4 != 0 rows
+def test_staged_host_path_multi_panel_bit_exact(mnk, name):
+    """Pageable numpy operands big enough for several output panels: the
+    staged rings (AG_HOST_STAGE, 4 MB slots, the output draining on its own
+    host thread) return exactly the device path's bits, through both the
+    numpy fast path (gemm_execute) and dispatch_native, with a fresh output
+    and with a caller-owned one."""
+    import torch
+    cfg = KernelConfig.from_canonical(name)
+    s = ProblemShape(*mnk, alpha=1.0, beta=0.5)
+    A, B, C = rand_operands(s, seed=sum(mnk))
+    caps = DeviceCaps.b200()
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+    ref, _ = gemm_execute(s, cfg, dA, dB, dC, caps)
+    ref = ref.cpu().numpy()
+    got, _ = gemm_execute(s, cfg, A, B, C, caps)
+    np.testing.assert_array_equal(got, ref)
+    out = np.full((s.M, s.N), np.nan, np.float32)
+    got2, _ = gemm_execute(s, cfg, A, B, C, caps, out=out)
+    assert got2 is out
+    np.testing.assert_array_equal(out, ref)
+    got3, picked, _ = codegen.dispatch_native(_one_class_selector(cfg), s, A, B, C, caps)
+    assert picked == cfg
+    np.testing.assert_array_equal(got3, ref)
