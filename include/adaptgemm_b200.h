@@ -177,6 +177,17 @@ int ag_gemm_host_ex(const ag_shape* shape, const ag_config* config, const ag_cap
  * (the reference's numpy-only package) drive the host path. */
 void* ag_device_scratch(size_t bytes);
 
+/* Caching pinned host allocator for host-path RESULTS (the fresh numpy
+ * output of gemm_execute(..., out=None), kernels.py:328-349): page-locked
+ * (cudaHostAllocPortable) blocks in 2 MB size classes, reused after
+ * ag_host_free, at most AG_HOST_CACHE_BYTES (env, default 4 GiB) kept
+ * cached.  A result written into such a block arrives by DMA with no
+ * staging copy and no first-touch page faults.  NULL when pinning fails
+ * (the caller then allocates pageable memory). */
+void* ag_host_alloc(size_t bytes);
+void ag_host_free(void* p);
+size_t ag_host_cache_bytes(void); /* bytes cached (free) right now */
+
 /* ag_gemm timed on the device: `warmup` untimed runs then `repeats` timed
  * samples (CUDA events on `stream`); each sample is the mean of `inner`
  * back-to-back runs replayed from one CUDA graph (inner <= 0: chosen so a

@@ -91,6 +91,9 @@ SIGNATURES = {
     "ag_gemm_host": (c_int, _GEMM_ARGS[:-1] + [c_int, _P]),
     "ag_gemm_host_ex": (c_int, _GEMM_ARGS[:-1] + [c_int, c_int, _P, POINTER(c_double)]),
     "ag_device_scratch": (c_void_p, [c_size_t]),
+    "ag_host_alloc": (c_void_p, [c_size_t]),
+    "ag_host_free": (None, [c_void_p]),
+    "ag_host_cache_bytes": (c_size_t, []),
     "ag_dispatch_gemm_host_ex": (c_int, [c_void_p, POINTER(AgConfig), POINTER(AgShape), POINTER(AgCaps), c_int,
                                          _P, c_int64, _P, c_int64, _P, c_int64, _P, c_int64, _P, c_size_t, c_int,
                                          c_int, _P, POINTER(AgConfig), POINTER(c_int), POINTER(c_double)]),

@@ -9,8 +9,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <condition_variable>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -599,6 +601,71 @@ size_t ag_host_scratch_bytes(const ag_shape* s, const ag_config* c, int dtype, i
     HostPlan h;
     plan_host(s, c, dtype, panels, &h);
     return h.total;
+}
+
+// caching pinned host allocator (results of the numpy path)
+namespace {
+struct HostCache {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_blocks;  // size class -> block
+    std::unordered_map<void*, size_t> sizes;   // every block this cache owns
+    size_t cached = 0, cap = (size_t)4 << 30;
+    HostCache() {
+        if (const char* e = std::getenv("AG_HOST_CACHE_BYTES")) cap = (size_t)std::strtoull(e, nullptr, 10);
+    }
+};
+HostCache& host_cache() {
+    static HostCache* c = new HostCache();  // never destroyed: blocks may be freed during interpreter teardown
+    return *c;
+}
+}  // namespace
+
+void* ag_host_alloc(size_t bytes) {
+    if (!bytes) return nullptr;
+    constexpr size_t kClass = 2u << 20;
+    const size_t sz = (bytes + kClass - 1) / kClass * kClass;
+    HostCache& hc = host_cache();
+    {
+        std::lock_guard<std::mutex> lk(hc.mu);
+        auto it = hc.free_blocks.lower_bound(sz);
+        if (it != hc.free_blocks.end() && it->first <= sz + sz / 2) {  // at most 1.5x the request
+            void* p = it->second;
+            hc.cached -= it->first;
+            hc.free_blocks.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, sz, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(hc.mu);
+    hc.sizes[p] = sz;
+    return p;
+}
+
+void ag_host_free(void* p) {
+    if (!p) return;
+    HostCache& hc = host_cache();
+    std::lock_guard<std::mutex> lk(hc.mu);
+    auto s = hc.sizes.find(p);
+    if (s == hc.sizes.end()) return;
+    hc.free_blocks.emplace(s->second, p);
+    hc.cached += s->second;
+    while (hc.cached > hc.cap && !hc.free_blocks.empty()) {  // drop the largest cached blocks first
+        auto last = std::prev(hc.free_blocks.end());
+        cudaFreeHost(last->second);
+        hc.cached -= last->first;
+        hc.sizes.erase(last->second);
+        hc.free_blocks.erase(last);
+    }
+}
+
+size_t ag_host_cache_bytes(void) {
+    HostCache& hc = host_cache();
+    std::lock_guard<std::mutex> lk(hc.mu);
+    return hc.cached;
 }
 
 void* ag_device_scratch(size_t bytes) {

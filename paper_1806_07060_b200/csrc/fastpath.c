@@ -4,9 +4,11 @@
  * gemm_execute(shape, config, A, B, C, caps, out) (kernels.py:328-349) with
  * numpy operands is: legality (ConfigError) -> operand checks (ShapeError,
  * kernels.py:271-283, same order and messages as kernels._check_operands)
- * -> ag_gemm_host_ex (H2D, family path, D2H in one blocking call, host
- * buffers page-locked for the call, the library's own device scratch) with
- * the GIL released -> (out, device seconds of the family path).
+ * -> ag_gemm_host_ex (H2D, family path, D2H in one blocking call; pageable
+ * operands staged through the library's pinned rings, AG_HOST_STAGE; the
+ * library's own device scratch) with the GIL released -> (out, device
+ * seconds of the family path).  A fresh result (out=None) of 1 MB or more is
+ * a numpy array over a block of the library's caching pinned allocator.
  *
  * Operands that are not plain row-major float32/float64 numpy arrays make
  * `execute` return NotImplemented; the Python path then handles them.
@@ -21,6 +23,7 @@
 static PyObject* ConfigError = NULL;
 static PyObject* ShapeError = NULL;
 static PyObject* np_empty = NULL;
+static PyObject* np_frombuffer = NULL;
 static PyObject* np_f32 = NULL;
 static PyObject* np_f64 = NULL;
 
@@ -82,6 +85,74 @@ static int read_caps(PyObject* o, ag_caps* k) {
     k->max_threads = PyLong_AsLongLong(x);
     Py_DECREF(x);
     return (k->max_threads == -1 && PyErr_Occurred()) ? -1 : 0;
+}
+
+/* A page-locked block from the library's caching host allocator
+ * (ag_host_alloc), exported through the buffer protocol: the numpy result of
+ * an out=None call lives in one, so the D2H lands by DMA with no staging
+ * copy and no page faults; freeing the array returns the block to the cache. */
+typedef struct {
+    PyObject_HEAD
+    void* p;
+    Py_ssize_t n;
+} PinnedBlock;
+
+static int pb_getbuffer(PyObject* self, Py_buffer* view, int flags) {
+    PinnedBlock* b = (PinnedBlock*)self;
+    return PyBuffer_FillInfo(view, self, b->p, b->n, 0, flags);
+}
+static void pb_dealloc(PyObject* self) {
+    ag_host_free(((PinnedBlock*)self)->p);
+    Py_TYPE(self)->tp_free(self);
+}
+static PyBufferProcs pb_buffer = {pb_getbuffer, NULL};
+static PyTypeObject PinnedBlockType = {
+    PyVarObject_HEAD_INIT(NULL, 0)
+    .tp_name = "_fastpath.PinnedBlock",
+    .tp_basicsize = sizeof(PinnedBlock),
+    .tp_dealloc = pb_dealloc,
+    .tp_as_buffer = &pb_buffer,
+    .tp_flags = Py_TPFLAGS_DEFAULT,
+    .tp_doc = "page-locked result block (ag_host_alloc)",
+};
+
+#define PINNED_OUT_MIN (1 << 20) /* smaller results: np.empty (a pageable copy costs less than a block) */
+
+/* a fresh m x n result: pinned when large enough and the cache can pin it,
+ * else np.empty */
+static PyObject* new_result(int64_t m, int64_t n, int code) {
+    const size_t nbytes = (size_t)(m * n) * (code == 0 ? 4 : 8);
+    PyObject* dtype = code == 0 ? np_f32 : np_f64;
+    if (nbytes >= PINNED_OUT_MIN) {
+        void* p = ag_host_alloc(nbytes);
+        if (p) {
+            PinnedBlock* blk = PyObject_New(PinnedBlock, &PinnedBlockType);
+            if (!blk) {
+                ag_host_free(p);
+                return NULL;
+            }
+            blk->p = p;
+            blk->n = (Py_ssize_t)nbytes;
+            PyObject* flat = PyObject_CallFunctionObjArgs(np_frombuffer, (PyObject*)blk, dtype, NULL);
+            Py_DECREF(blk);
+            if (!flat) return NULL;
+            PyObject* arr = PyObject_CallMethod(flat, "reshape", "(LL)", (long long)m, (long long)n);
+            Py_DECREF(flat);
+            return arr;
+        }
+    }
+    PyObject* dims = Py_BuildValue("(LL)", (long long)m, (long long)n);
+    if (!dims) return NULL;
+    PyObject* arr = PyObject_CallFunctionObjArgs(np_empty, dims, dtype, NULL);
+    Py_DECREF(dims);
+    return arr;
+}
+
+/* cache_bytes() -> bytes the pinned result cache holds free (ag_host_cache_bytes) */
+static PyObject* fp_cache_bytes(PyObject* self, PyObject* unused) {
+    (void)self;
+    (void)unused;
+    return PyLong_FromSize_t(ag_host_cache_bytes());
 }
 
 /* a 2-D float32 / float64 buffer; dtype code 0 / 1, -1 other, -2 not a buffer */
@@ -208,10 +279,7 @@ static PyObject* fp_execute(PyObject* self, PyObject* const* args, Py_ssize_t na
     }
     PyObject* dst;
     if (out == Py_None) {
-        PyObject* dims = Py_BuildValue("(LL)", (long long)s.m, (long long)s.n);
-        if (!dims) goto done;
-        dst = PyObject_CallFunctionObjArgs(np_empty, dims, a.code == 0 ? np_f32 : np_f64, NULL);
-        Py_DECREF(dims);
+        dst = new_result(s.m, s.n, a.code);
         if (!dst) goto done;
     } else {
         dst = Py_NewRef(out);
@@ -278,6 +346,7 @@ static PyMethodDef methods[] = {
     {"execute", (PyCFunction)(void (*)(void))fp_execute, METH_FASTCALL, "gemm_execute over numpy operands"},
     {"legal", (PyCFunction)(void (*)(void))fp_legal, METH_FASTCALL, "ag_is_legal(config, caps)"},
     {"set_errors", (PyCFunction)(void (*)(void))fp_set_errors, METH_FASTCALL, "bind the exception classes"},
+    {"cache_bytes", fp_cache_bytes, METH_NOARGS, "bytes held free by the pinned result cache"},
     {NULL, NULL, 0, NULL},
 };
 
@@ -296,10 +365,12 @@ PyMODINIT_FUNC PyInit__fastpath(void) {
     PyObject* np = PyImport_ImportModule("numpy");
     if (!np) return NULL;
     np_empty = PyObject_GetAttrString(np, "empty");
+    np_frombuffer = PyObject_GetAttrString(np, "frombuffer");
     np_f32 = PyObject_GetAttrString(np, "float32");
     np_f64 = PyObject_GetAttrString(np, "float64");
     Py_DECREF(np);
-    if (!np_empty || !np_f32 || !np_f64) return NULL;
+    if (!np_empty || !np_frombuffer || !np_f32 || !np_f64) return NULL;
+    if (PyType_Ready(&PinnedBlockType) < 0) return NULL;
     ConfigError = Py_NewRef(PyExc_ValueError);
     ShapeError = Py_NewRef(PyExc_ValueError);
     return PyModule_Create(&module);

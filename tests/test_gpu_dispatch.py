@@ -373,3 +373,39 @@ def test_staged_host_path_multi_panel_bit_exact(mnk, name):
     got3, picked, _ = codegen.dispatch_native(_one_class_selector(cfg), s, A, B, C, caps)
     assert picked == cfg
     np.testing.assert_array_equal(got3, ref)
+
+
+def test_pinned_result_blocks_are_cached_and_exact():
+    """A fresh result of >= 1 MB lives in a block of the library's caching
+    pinned allocator (ag_host_alloc): a plain, writable numpy array with the
+    device path's bits; dropping it returns the block to the cache and the
+    next call of that size reuses it."""
+    import gc
+
+    import torch
+
+    from paper_1806_07060_b200 import _native
+    fp = pytest.importorskip("paper_1806_07060_b200._fastpath")
+    cfg = KernelConfig.from_canonical("indirect:64-64-16-8-4-1")
+    s = ProblemShape(1024, 1024, 64)
+    A, B, C = rand_operands(s, seed=3)
+    ref, _ = gemm_execute(s, cfg, *(torch.from_numpy(x).cuda() for x in (A, B, C)))
+    out, _ = gemm_execute(s, cfg, A, B, C)
+    assert isinstance(out, np.ndarray) and out.shape == (1024, 1024) and out.flags.writeable
+    owner, chain = out, []
+    while owner is not None:  # ndarray views -> frombuffer array -> (memoryview ->) PinnedBlock
+        chain.append(type(owner).__name__)
+        owner = getattr(owner, "base", None) if not isinstance(owner, memoryview) else owner.obj
+    assert "PinnedBlock" in chain, chain
+    np.testing.assert_array_equal(out, ref.cpu().numpy())
+    out[0, 0] = 1.0  # an ordinary array for the caller
+    before = fp.cache_bytes()
+    del out
+    gc.collect()
+    assert fp.cache_bytes() >= before + 4 * 1024 * 1024
+    again, _ = gemm_execute(s, cfg, A, B, C)
+    assert fp.cache_bytes() == before
+    np.testing.assert_array_equal(again, ref.cpu().numpy())
+    assert _native.lib().ag_host_cache_bytes() == fp.cache_bytes()
+    small, _ = gemm_execute(ProblemShape(64, 64, 64), cfg, *rand_operands(ProblemShape(64, 64, 64), seed=4))
+    assert small.base is None  # under 1 MB: np.empty
