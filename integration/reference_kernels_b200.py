@@ -23,6 +23,7 @@ library's pinned staging rings (AG_HOST_STAGE).
 """
 import ctypes
 import os
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -78,6 +79,10 @@ def lib():
                                       ctypes.c_int, _P, _I, _P, _I, _P, _I, _P, _I, _P, ctypes.c_size_t, ctypes.c_int,
                                       ctypes.c_int, _P, ctypes.POINTER(ctypes.c_double)]
         L.ag_gemm_host_ex.restype = ctypes.c_int
+        L.ag_host_alloc.argtypes = [ctypes.c_size_t]
+        L.ag_host_alloc.restype = ctypes.c_void_p
+        L.ag_host_free.argtypes = [ctypes.c_void_p]
+        L.ag_host_free.restype = None
         _lib = L
     return _lib
 
@@ -108,6 +113,20 @@ def _check_operands(shape, A, B, C):
         raise ShapeError(f"unsupported dtype {A.dtype}, want float32 or float64")
 
 
+def _pinned_result(L, m, n, dtype):
+    """A fresh m x n result (kernels.py:286-288) in a block of the library's
+    caching pinned allocator (ag_host_alloc), so the D2H lands by DMA; the
+    block goes back to the cache when the array is collected.  Small results
+    (or a failed pin) are plain np.empty."""
+    nbytes = m * n * np.dtype(dtype).itemsize
+    p = L.ag_host_alloc(nbytes) if nbytes >= (1 << 20) else None
+    if not p:
+        return np.empty((m, n), dtype=dtype)
+    raw = (ctypes.c_char * nbytes).from_address(p)
+    weakref.finalize(raw, L.ag_host_free, p)
+    return np.frombuffer(raw, dtype=dtype).reshape(m, n)
+
+
 def gemm_execute(shape, config, A, B, C, caps, out=None):
     """kernels.gemm_execute (kernels.py:328-349) on the B200."""
     L = lib()
@@ -117,7 +136,7 @@ def gemm_execute(shape, config, A, B, C, caps, out=None):
     _check_operands(shape, A, B, C)
     A, B, C = (np.ascontiguousarray(x) for x in (A, B, C))
     if out is None:
-        out = np.empty((shape.M, shape.N), dtype=A.dtype)
+        out = _pinned_result(L, shape.M, shape.N, A.dtype)
     elif out.shape != (shape.M, shape.N) or out.dtype != A.dtype:
         raise ShapeError("out buffer has wrong shape or dtype")
     dst = out if out.flags.c_contiguous else np.empty_like(out, order="C")

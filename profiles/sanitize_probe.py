@@ -24,6 +24,10 @@ CASES = [
     ((130, 70, 100), "tma:128-128-32-8-8-1"),
     ((300, 260, 200), "bf16:256-128-64-4-1-1"),    # tcgen05 CTA pair
     ((300, 260, 200), "tf32:128-64-32-4-1-1"),
+    ((300, 260, 600), "tf32x3:128-128-32-3-1-1"),  # 3xTF32, 3 TMEM chunks, running sum
+    ((300, 260, 600), "tf32x3:256-64-32-3-1-1"),   # 3xTF32 CTA pair
+    ((1000, 16, 1024), "skinny_n:64-16-32-2-4-4"),  # skinny_n, 4-CTA cluster reduction
+    ((35, 1001, 512), "skinny_m:40-256-32-1-2-4"),  # skinny_m, N % 4 != 0
 ]
 
 
@@ -43,6 +47,13 @@ def main():
     A, B, C = (rng.uniform(-1, 1, d).astype(np.float32) for d in ((700, 128), (128, 300), (700, 300)))
     codegen.dispatch_native(sel, s, A, B, C, caps, panels=3)
     print("host path ok", flush=True)
+    # staged host path: pageable numpy through the pinned rings, 4 panels, the
+    # output draining on its own host thread, the result in a pinned block
+    s = ProblemShape(2048, 2048, 1024)
+    A, B, C = (rng.uniform(-1, 1, d).astype(np.float32) for d in ((2048, 1024), (1024, 2048), (2048, 2048)))
+    out, _ = gemm_execute(s, KernelConfig.from_canonical("indirect:64-64-32-8-8-1"), A, B, C, caps)
+    ref = A[:64].astype(np.float64) @ B.astype(np.float64)
+    print(f"staged host path rf={np.linalg.norm(out[:64] - ref) / np.linalg.norm(ref):.1e}", flush=True)
 
 
 if __name__ == "__main__":

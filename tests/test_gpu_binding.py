@@ -2,6 +2,7 @@
 the reference's `gemm_execute` convention through the C-ABI -- numpy in,
 numpy out, the reference's exception order -- against the reference's own
 golden outputs (tests/golden, produced by /root/reference itself)."""
+import ctypes
 import importlib.util
 
 import numpy as np
@@ -60,11 +61,22 @@ def test_binding_error_order(binding):
 
 
 def test_binding_large_pageable_call(binding):
-    """A call big enough to page-lock and pipeline (>= 32 MB moved)."""
+    """A call big enough to stage and pipeline (>= 32 MB moved): pageable
+    operands through the pinned rings, the fresh result in a cached pinned
+    block that returns to the cache when the array is collected."""
+    import gc
     from paper_1806_07060_b200.tuner import _bench_buffers
     s = ProblemShape(2048, 3000, 1024)
     A, B, C, _ = _bench_buffers(s, np.float32, 0)
-    out, sec = binding.gemm_execute(s, KernelConfig.from_canonical("indirect:64-64-16-8-4-2"), A, B, C,
-                                    DeviceCaps())
+    cfg = KernelConfig.from_canonical("indirect:64-64-16-8-4-2")
+    out, sec = binding.gemm_execute(s, cfg, A, B, C, DeviceCaps())
     exact = A.astype(np.float64) @ B.astype(np.float64)
     assert rel_frobenius(out, exact) <= 1e-5 and sec > 0
+    L = binding.lib()
+    L.ag_host_cache_bytes.restype = ctypes.c_size_t
+    before = L.ag_host_cache_bytes()
+    del out
+    gc.collect()
+    assert L.ag_host_cache_bytes() >= before + 2048 * 3000 * 4
+    again, _ = binding.gemm_execute(s, cfg, A, B, C, DeviceCaps())
+    assert rel_frobenius(again, exact) <= 1e-5
