@@ -752,7 +752,10 @@ def run_ours(args):
                        "operands and the fresh output cross through pinned staging rings filled / drained by "
                        "parallel host copies, H2D / family path / D2H pipelined over output panels on three "
                        "streams; median of 3 wall-clock calls per shape",
-                "pinned_dispatch_native": round(e2e_pinned * world, 2)},
+                "pinned_dispatch_native": round(e2e_pinned * world, 2),
+                "per_shape_ms": [[list(c.shape.mnk), round(t * 1e3, 3), round(u * 1e3, 3)]
+                                 for c, t, u in zip(cases, e2e_t, pinned_t)],
+                "per_shape_columns": ["mnk", "numpy_dispatch_and_run_ms", "pinned_dispatch_native_ms"]},
         "roofline": {"bound": "fp32-cuda-core (compute)", "achieved": round(achieved, 3),
                      "peak": round(peak_meas, 3), "unit": "TFLOP/s", "frac": round(achieved / peak_meas, 4),
                      "traffic": traffic, "kernel": key,

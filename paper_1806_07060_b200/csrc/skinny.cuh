@@ -258,11 +258,15 @@ struct MShape {
     static constexpr size_t SMEM = 1024 + (RING > PART ? RING : PART) + 2 * D * 8 + 64;
 };
 
-template <int BM, int TN2, int NW, int D>
-__global__ void __launch_bounds__(NW * 32, NW == 4 ? 3 : 1)
+// B streams through registers in QK-k granules, NBUF granule buffers deep
+// (NBUF - 1 granules in flight ahead of the FMAs; NBUF divides BK / QK so
+// every buffer index is a compile-time constant).
+template <int BM, int TN2, int NW, int D, int QK = 8, int NBUF = 2>
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? (NBUF > 2 ? 2 : 3) : 1)
 skinny_m_kernel(const __grid_constant__ CUtensorMap mapA, const Params p) {
     using S_ = MShape<BM, TN2, NW, D>;
-    constexpr int NT = S_::NT, BNC = S_::BNC, RS = S_::RS, QK = 8;  // B prefetch granule: 8 k
+    constexpr int NT = S_::NT, BNC = S_::BNC, RS = S_::RS;
+    static_assert((BK / QK) % NBUF == 0 && QK % 4 == 0, "granule ring");
     constexpr uint32_t A_BYTES = S_::A_BYTES;
     static_assert(BM % 4 == 0 && TN2 % 2 == 0, "tile");
 
@@ -305,8 +309,8 @@ skinny_m_kernel(const __grid_constant__ CUtensorMap mapA, const Params p) {
         cok[c] = gn < p.N;
         bcol[c] = p.B + (cok[c] ? gn : 0);
     }
-    // B granules (8 k x TN2) in registers, one granule ahead
-    float bq[2][QK][TN2];
+    // B granules (QK k x TN2) in registers, NBUF - 1 granules ahead
+    float bq[NBUF][QK][TN2];
     auto load_q = [&](int q, float (&dst)[QK][TN2]) {  // granule q of this slice (4 per K block)
         const int kbase = kb0 * BK + q * QK;
 #pragma unroll
@@ -324,7 +328,9 @@ skinny_m_kernel(const __grid_constant__ CUtensorMap mapA, const Params p) {
         for (int c = 0; c < TN2 / 2; ++c) acc[m][c] = 0ull;
 
     constexpr int QPB = BK / QK;  // granules per K block
-    if (nk > 0) load_q(0, bq[0]);
+#pragma unroll
+    for (int g = 0; g < NBUF - 1; ++g)
+        if (g < QPB * nk) load_q(g, bq[g]);
     for (int j = 0; j < nk; ++j) {
         const int s = j % D;
         if (tid == 0) {  // refill the slot of block j - 1 with block j + D - 1
@@ -339,8 +345,8 @@ skinny_m_kernel(const __grid_constant__ CUtensorMap mapA, const Params p) {
 #pragma unroll
         for (int h = 0; h < QPB; ++h) {
             const int qq = QPB * j + h;
-            if (qq + 1 < QPB * nk) load_q(qq + 1, bq[(h + 1) & 1]);
-            const float(&b)[QK][TN2] = bq[h & 1];
+            if (qq + NBUF - 1 < QPB * nk) load_q(qq + NBUF - 1, bq[(h + NBUF - 1) % NBUF]);
+            const float(&b)[QK][TN2] = bq[h % NBUF];
 #pragma unroll
             for (int k4 = 0; k4 < QK; k4 += 4) {
                 f32x2 bp[4][TN2 / 2];
@@ -491,7 +497,7 @@ int launch_n(const GemmCall& c) {
 }
 
 // skinny_m:bm-bn-32-1-tn2-slices, bn = 32 nw tn2
-template <int BM, int TN2, int NW>
+template <int BM, int TN2, int NW, int QK = 8, int NBUF = 2>
 int launch_m(const GemmCall& c) {
     constexpr int D = 4;
     using S_ = MShape<BM, TN2, NW, D>;
@@ -509,7 +515,8 @@ int launch_m(const GemmCall& c) {
         return fail(c, AG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     static SmemGrant granted;
     static PerDevice<int> np_ok;
-    return launch_sliced(c, skinny_m_kernel<BM, TN2, NW, D>, granted, np_ok, S_::SMEM, S_::NT, tiles_m * tiles_n,
+    return launch_sliced(c, skinny_m_kernel<BM, TN2, NW, D, QK, NBUF>, granted, np_ok, S_::SMEM, S_::NT,
+                         tiles_m * tiles_n,
                          slices, mA, p);
 }
 

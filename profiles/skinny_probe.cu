@@ -12,9 +12,12 @@ using namespace ag;
 struct Exp { int kind, a, b, c; LaunchFn fn; };  // kind 0: skinny_n<TM,BN,NW>, 1: skinny_m<BM,TN2,NW>
 #define N_LIST(X) X(1, 16, 4) X(1, 16, 8) X(2, 16, 4) X(2, 16, 8) X(4, 16, 4) X(1, 32, 4) X(1, 32, 8) X(2, 32, 4) X(2, 32, 8) X(1, 64, 4) X(1, 64, 8)
 #define M_LIST(X) X(40, 2, 4) X(40, 2, 8) X(48, 2, 4) X(24, 2, 4) X(16, 4, 4) X(32, 2, 4) X(16, 2, 4) X(8, 4, 4)
+// kind 2: skinny_m<40, 2, NW> with the B granule ring varied: (QK k per granule, NBUF buffers)
+#define M2_LIST(X) X(8, 4, 4) X(4, 4, 4) X(4, 8, 4) X(8, 2, 8) X(8, 4, 8) X(4, 8, 8)
 #define N_ENTRY(a, b, c) {0, a, b, c, &skinny::launch_n<a, b, c>},
 #define M_ENTRY(a, b, c) {1, a, b, c, &skinny::launch_m<a, b, c>},
-static const Exp kExps[] = {N_LIST(N_ENTRY) M_LIST(M_ENTRY)};
+#define M2_ENTRY(qk, nb, nw) {2, qk, nb, nw, &skinny::launch_m<40, 2, nw, qk, nb>},
+static const Exp kExps[] = {N_LIST(N_ENTRY) M_LIST(M_ENTRY) M2_LIST(M2_ENTRY)};
 
 extern "C" int exp_count() { return (int)(sizeof(kExps) / sizeof(kExps[0])); }
 extern "C" void exp_info(int i, int* t) { t[0] = kExps[i].kind; t[1] = kExps[i].a; t[2] = kExps[i].b; t[3] = kExps[i].c; }
