@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -698,6 +699,24 @@ int ag_gemm_host(const ag_shape* s, const ag_config* c, const ag_caps* caps, int
 int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, int dtype, const void* A,
                     int64_t lda, const void* B, int64_t ldb, const void* C, int64_t ldc, void* out, int64_t ldo,
                     void* dev, size_t dev_bytes, int panels, int flags, void* stream, double* kernel_seconds) {
+    // AG_HOST_TRACE=1: one stderr line per call with the host-side phase times (us)
+    static const bool tracing = std::getenv("AG_HOST_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    std::string trace_line;
+    auto mark = [&](const char* what) {
+        if (!tracing) return;
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count();
+        char buf[64];
+        snprintf(buf, sizeof buf, " %s=%.0f", what, us);
+        trace_line += buf;
+    };
+    struct TraceOut {
+        const bool& on;
+        std::string& line;
+        ~TraceOut() {
+            if (on) fprintf(stderr, "[ag_host]%s\n", line.c_str());
+        }
+    } trace_out{tracing, trace_line};
     ag::LaunchFn fn = nullptr;
     int r = prepare(s, c, caps, dtype, A, lda, B, ldb, C, ldc, out, ldo, &fn);
     if (r) return r;
@@ -764,7 +783,7 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
             char* ostage = stage + ((in_b + 255) / 256) * 256;
             if (ostage + o_b > stage + (4u << 20)) ostage = stage;  // inputs are consumed before the D2H lands
             ok(cudaMemcpyAsync(ostage, dO, o_b, cudaMemcpyDeviceToHost, run));
-            ok(cudaStreamSynchronize(run));
+            ok(ag::hoststage::spin_stream(run));
             if (ce != cudaSuccess) return set_err(AG_ERR_CUDA, std::string("host path: ") + cudaGetErrorString(ce));
             char* op = static_cast<char*>(out);
             for (int64_t rr = 0; rr < M; ++rr) memcpy(op + rr * ldo * e, ostage + rr * N * e, (size_t)(N * e));
@@ -777,6 +796,7 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
             return le == cudaSuccess ? AG_OK : set_err(AG_ERR_CUDA, cudaGetErrorString(le));
         }
     }
+    mark("plan");
     HostLocks locks;
     if (flags & AG_HOST_REGISTER) {
         locks.lock(A, h.ra, lda, h.ca, h.elem);
@@ -826,6 +846,7 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
     } else {
         put(pin_a, dA, h.ca * e, A, lda * e, h.ca * e, h.ra);
     }
+    mark("first_operand");
     // panel p's output back to the host (after its family path)
     auto drain = [&](int p, cudaError_t& err) {
         const int64_t x0 = (int64_t)p * h.chunk, w = std::min(h.chunk, h.extent - x0);
@@ -908,6 +929,7 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
             po = dO + x0 * e;
             ps.n = w;
         }
+        mark("panel_in");
         ok(cudaEventRecord(ein, in));
         ok(cudaStreamWaitEvent(run, ein, 0));
         cudaEvent_t k0 = kernel_seconds ? t_pipe.timing_event(2 * p) : nullptr;
@@ -930,15 +952,18 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
             drain(p - 1, ce);  // the previous panel's output drains while this panel computes
         }
     }
+    mark("launched");
     if (drain_thread) {
         drainer.join();
         ok(drain_err);
     } else {
         drain(h.panels - 1, ce);
     }
-    ok(cudaStreamSynchronize(back));
-    ok(cudaStreamSynchronize(run));
-    ok(cudaStreamSynchronize(in));
+    mark("drained");
+    ok(ag::hoststage::spin_stream(back));
+    ok(ag::hoststage::spin_stream(run));
+    ok(ag::hoststage::spin_stream(in));
+    mark("synced");
     if (ce != cudaSuccess) return set_err(AG_ERR_CUDA, std::string("host path: ") + cudaGetErrorString(ce));
     if (kernel_seconds) {  // device time of the family path, summed over the panels
         double sum = 0.0;

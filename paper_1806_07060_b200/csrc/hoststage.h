@@ -155,6 +155,30 @@ inline void copy_rows(char* dst, int64_t dpitch, const char* src, int64_t spitch
     });
 }
 
+// Spin on a CUDA event / stream instead of the runtime's synchronize: the
+// runtime may block the thread and wake it through the OS (tens of
+// microseconds per wait on this box), and a host-path call waits several
+// times on short DMAs.
+inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+}
+inline cudaError_t spin_event(cudaEvent_t e) {
+    for (;;) {
+        const cudaError_t r = cudaEventQuery(e);
+        if (r != cudaErrorNotReady) return r;
+        cpu_relax();
+    }
+}
+inline cudaError_t spin_stream(cudaStream_t st) {
+    for (;;) {
+        const cudaError_t r = cudaStreamQuery(st);
+        if (r != cudaErrorNotReady) return r;
+        cpu_relax();
+    }
+}
+
 inline bool is_pinned(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -233,7 +257,7 @@ inline cudaError_t h2d(Ring& ring, Block b, cudaStream_t st) {
         const int s = ring.next;
         ring.next = (ring.next + 1) % Ring::kSlots;
         if (ring.busy[s]) {
-            cudaError_t e = cudaEventSynchronize(ring.ev[s]);
+            cudaError_t e = spin_event(ring.ev[s]);
             if (e != cudaSuccess) return e;
         }
         char* slot = ring.slot(s);
@@ -254,7 +278,7 @@ inline cudaError_t d2h(Ring& ring, Block b, cudaStream_t st) {
     if (b.width > (int64_t)Ring::kSlotBytes && !(b.hpitch == b.width && b.dpitch == b.width)) {
         cudaError_t e = cudaMemcpy2DAsync(b.host, (size_t)b.hpitch, b.dev, (size_t)b.dpitch, (size_t)b.width,
                                           (size_t)b.rows, cudaMemcpyDeviceToHost, st);
-        return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+        return e != cudaSuccess ? e : spin_stream(st);
     }
     const std::vector<Chunk> cs = chunks_of(b);
     const int n = (int)cs.size();
@@ -272,7 +296,7 @@ inline cudaError_t d2h(Ring& ring, Block b, cudaStream_t st) {
     for (int i = 0; i < n; ++i) {
         const Chunk& c = cs[i];
         const int s = i % Ring::kSlots;
-        cudaError_t e = cudaEventSynchronize(ring.ev[s]);
+        cudaError_t e = spin_event(ring.ev[s]);
         if (e != cudaSuccess) return e;
         copy_rows(b.host + c.r0 * b.hpitch + c.b0, b.hpitch, ring.slot(s), c.nb, c.nb, c.nr);
         if (i + Ring::kSlots < n && (e = issue(i + Ring::kSlots)) != cudaSuccess) return e;

@@ -272,10 +272,12 @@ int launch_inplace(const GemmCall& c) {
 // AROW_OK (split-K family launchers): when op(A) is the caller's row-major
 // A and M, K are tile multiples, run the AROW core that reads A in place
 // instead of transpose-packing it.
-template <typename T, int BM, int BN, int BK, int TM, int TN, int UK, bool AROW_OK = false>
+// STAGES_OVERRIDE (experiments only, profiles/exp_tiles.cu): the cp.async
+// ring depth instead of tiled_stages' choice.
+template <typename T, int BM, int BN, int BK, int TM, int TN, int UK, bool AROW_OK = false, int STAGES_OVERRIDE = 0>
 int launch_indirect(const GemmCall& c) {
     constexpr bool FIXED = BM > 0 && BN > 0 && BK > 0;
-    constexpr int STAGES = tiled_stages<T>(BM, BN, BK);
+    constexpr int STAGES = STAGES_OVERRIDE ? STAGES_OVERRIDE : tiled_stages<T>(BM, BN, BK);
     constexpr int STAGES_AROW = tiled_stages<T>(BM + a_pad<T, true>(), BN, BK);
     constexpr int VL = FIXED ? VecW<T>::W : 1;
     constexpr int WB = FragW<T, TN>::W;

@@ -48,11 +48,31 @@ using namespace ag;
     X(128, 128, 32, 8, 16, 9) \
     X(128, 128, 32, 16, 8, 9)
 
+// ring-depth variants of the shipped big tiles: uk field = uk + 100 * stages
+#define STAGE_LIST(X)              \
+    X(64, 128, 32, 8, 8, 2, 2)     \
+    X(64, 128, 32, 8, 8, 2, 3)     \
+    X(64, 128, 32, 8, 8, 2, 4)     \
+    X(64, 128, 32, 8, 8, 2, 5)     \
+    X(128, 64, 32, 8, 8, 2, 3)     \
+    X(64, 128, 16, 8, 8, 2, 4)     \
+    X(64, 128, 16, 8, 8, 2, 6)     \
+    X(128, 128, 16, 16, 8, 1, 2)   \
+    X(128, 128, 16, 16, 8, 1, 3)   \
+    X(128, 128, 16, 16, 8, 1, 4)   \
+    X(128, 256, 32, 8, 16, 1, 2)   \
+    X(128, 256, 32, 8, 16, 1, 3)   \
+    X(128, 256, 16, 8, 16, 1, 3)   \
+    X(128, 256, 16, 8, 16, 1, 5)
+
 struct Exp { int bm, bn, bk, tm, tn, uk; LaunchFn fn; };
 #define EXP_ENTRY(bm, bn, bk, tm, tn, uk) {bm, bn, bk, tm, tn, uk, &launch_indirect<float, bm, bn, bk, tm, tn, uk>},
 #define INPLACE_ENTRY(bm, bn, bk, tm, tn, uk) {bm, bn, bk, tm, tn, uk, &launch_inplace<bm, bn, bk, tm, tn>},
 #define TMA_ENTRY(bm, bn, bk, tm, tn, uk) {bm, bn, bk, tm, tn, uk, &f32tma::launch_tma<bm, bn, tm, tn>},
-static const Exp kExps[] = {EXP_LIST(EXP_ENTRY) INPLACE_LIST(INPLACE_ENTRY) TMA_LIST(TMA_ENTRY)};
+#define STAGE_ENTRY(bm, bn, bk, tm, tn, uk, st) \
+    {bm, bn, bk, tm, tn, uk + 100 * st, &launch_indirect<float, bm, bn, bk, tm, tn, uk, false, st>},
+static const Exp kExps[] = {EXP_LIST(EXP_ENTRY) INPLACE_LIST(INPLACE_ENTRY) TMA_LIST(TMA_ENTRY)
+                                STAGE_LIST(STAGE_ENTRY)};
 
 extern "C" int exp_count() { return (int)(sizeof(kExps) / sizeof(kExps[0])); }
 extern "C" void exp_tile(int i, int* t) {

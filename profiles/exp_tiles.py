@@ -42,13 +42,17 @@ def main():
         t = (ctypes.c_int * 6)()
         L.exp_tile(i, t)
         tiles.append("-".join(map(str, t)))
-    for (m, nn, k) in SHAPES:
+    only_stage = os.environ.get("EXP_STAGES")  # only the ring-depth variants (uk field >= 100)
+    shapes = [(5124, 9124, 2560), (4096, 7000, 4096), (2560, 7000, 2560), (8192, 8192, 8192)] if only_stage else SHAPES
+    for (m, nn, k) in shapes:
         a = torch.rand(m, k, device="cuda") - 0.5
         b = torch.rand(k, nn, device="cuda") - 0.5
         out = torch.empty(m, nn, device="cuda")
         ref = None
         res = {}
         for i in range(n):
+            if only_stage and int(tiles[i].split("-")[-1]) < 100:
+                continue
             ws_n = L.exp_ws(i, m, nn, k, 1)
             ws = torch.empty(ws_n, dtype=torch.uint8, device="cuda")
             sec = ctypes.c_double()
