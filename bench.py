@@ -647,7 +647,7 @@ def run_ours(args):
         A, B, C = c.host
         codegen.dispatch_and_run(tree, c.shape, A, B, C, caps, classes=classes)  # warm (selector, page-lock path)
         ts = []
-        for _ in range(3):
+        for _ in range(5):
             t0 = time.perf_counter()
             res = codegen.dispatch_and_run(tree, c.shape, A, B, C, caps, classes=classes)
             ts.append(time.perf_counter() - t0)
@@ -751,7 +751,7 @@ def run_ours(args):
                        "compiled numpy path (csrc/fastpath.c) -> ag_gemm_host_ex(AG_HOST_STAGE): the pageable "
                        "operands and the fresh output cross through pinned staging rings filled / drained by "
                        "parallel host copies, H2D / family path / D2H pipelined over output panels on three "
-                       "streams; median of 3 wall-clock calls per shape",
+                       "streams; median of 5 wall-clock calls per shape",
                 "pinned_dispatch_native": round(e2e_pinned * world, 2),
                 "per_shape_ms": [[list(c.shape.mnk), round(t * 1e3, 3), round(u * 1e3, 3)]
                                  for c, t, u in zip(cases, e2e_t, pinned_t)],
@@ -905,9 +905,12 @@ def x3_section(cases, default_t, device, distributed, times, fallback, args):
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
         tf32_peak = float(peaks.get("bf16_tflops", 2250.0)) / 2
         ach = c.flops / dt_t[dom] / 1e12
+        key = f"{'x'.join(map(str, c.shape.mnk))}:{dt_cfgs[dom].canonical()}"
+        traffic = json.loads(TRAFFIC_FILE.read_text()).get(key) if TRAFFIC_FILE.exists() else None
         roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32_peak / 3, 1), "unit": "TFLOP/s",
-                "frac": round(ach / (tf32_peak / 3), 4), "kernel": f"{'x'.join(map(str, c.shape.mnk))}:"
-                                                                  f"{dt_cfgs[dom].canonical()}",
+                "frac": round(ach / (tf32_peak / 3), 4), "kernel": key, "traffic": traffic,
+                "traffic_note": "DRAM bytes of the tc_gemm launch alone (ncu --set full); the lo-part convert "
+                                "pass adds 8 B per operand element",
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 2 = tf32, / 3 products per K step",
                 "note": "event time covers the family path (lo-part convert pass included)"}
     fams = {}
