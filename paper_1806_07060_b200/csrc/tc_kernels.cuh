@@ -52,6 +52,7 @@ constexpr int KIND_TF32X3 = 2;  // fp32-accurate: 3 tf32 products over hi / lo o
 constexpr int BM = 128;          // UMMA M (cta_group::1): TMEM lane = output row
 constexpr int ROW_BYTES = 128;   // one K block = one 128-byte swizzle row
 constexpr int THREADS = 192;     // producer warp, MMA warp, 4 epilogue warps
+constexpr int THREADS_X3 = 320;  // + 4 converter warps (tf32x3: the lo parts are made in shared memory)
 constexpr int ACC_STAGES_MAX = 2;  // TMEM accumulator double buffer (when 2 buffers fit 512 columns)
 constexpr int X3_CHUNK_BLOCKS = 8;  // 3xTF32: K blocks (8 x 32 = 256 k) per TMEM accumulation chunk
 
@@ -79,11 +80,31 @@ template <> struct Elem<KIND_BF16> {
 // a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi: the dropped a_lo.b_lo and the
 // tf32 truncation of the lo parts are below 2^-20 |a||b| per product, so the
 // result meets the fp32 families' RF <= 1e-5 contract on the tensor pipe.
-// A stage holds [hi | lo] of each operand; the MMA issuer runs 3 tf32 MMAs
-// per K step into the same TMEM accumulator.
+// A stage holds [hi | lo] of each operand: TMA lands the caller's fp32 tile
+// (= hi as a tf32 MMA reads it), four converter warps write lo = x - hi next
+// to it in shared memory (no HBM convert pass, half the L2 -> SM bytes of
+// staging both parts), and the MMA issuer runs 3 tf32 MMAs per K step.
 template <> struct Elem<KIND_TF32X3> : Elem<KIND_TF32> {
     static constexpr int PARTS = 2;
 };
+// 3xTF32 split: hi = the bits a tf32 MMA reads (low 13 mantissa bits
+// cleared), lo = x - hi, exact in fp32
+__host__ __device__ __forceinline__ float tf32_hi(float x) {
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+#else
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u &= 0xFFFFE000u;
+    std::memcpy(&x, &u, 4);
+    return x;
+#endif
+}
+__host__ __device__ __forceinline__ float tf32_lo(float x) { return x - tf32_hi(x); }
+template <int KIND>
+constexpr int kernel_threads() {
+    return Elem<KIND>::PARTS == 2 ? THREADS_X3 : THREADS;
+}
 
 // ---------------------------------------------------------------- device PTX
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -278,14 +299,17 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) 
 // the leader CTA issues the MMAs for both, and each CTA's TMEM holds its
 // 128 output rows.  Per SM this halves the B traffic of a 128 x BN tile.
 template <int KIND, int BN, int STAGES, int CTAS>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(kernel_threads<KIND>(), 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo, TcParams p) {
     constexpr int BK = Elem<KIND>::BK;
     constexpr int PARTS = Elem<KIND>::PARTS;  // [hi | lo] per operand and stage for 3xTF32
     constexpr int BNC = BN / CTAS;  // B rows (N) staged by each CTA
     constexpr uint32_t A_BYTES = BM * ROW_BYTES, B_BYTES = BNC * ROW_BYTES;  // one part
-    constexpr uint32_t STAGE_TX = (A_BYTES + B_BYTES) * CTAS * PARTS;
+    // TMA bytes per stage: the raw fp32 tiles; 3xTF32 lands them on each CTA's
+    // own barrier (its converter warps wait there), the other kinds on the
+    // leader's (the pair's MMA issuer waits there)
+    constexpr uint32_t STAGE_TX = PARTS == 2 ? (A_BYTES + B_BYTES) : (A_BYTES + B_BYTES) * CTAS;
     // The tensor core's fp32 accumulation is not round-to-nearest: with exact
     // products (tf32-truncated inputs) its error grows linearly in K (RF
     // 6.0e-6 at K = 2560, 1.9e-5 at 8192, 7.7e-5 at 32768, against 0.9e-6 /
@@ -319,7 +343,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + ACC_STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC_STAGES);
+    uint64_t* lo_full = tempty + ACC_STAGES;  // 3xTF32: lo parts of a stage written (converter warps, all CTAs)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lo_full + STAGES);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = CTAS == 2 ? cluster_rank() : 0;
@@ -339,6 +364,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4 * CTAS);  // one arrival per epilogue warp of every CTA
         }
+        if constexpr (PARTS == 2)
+            for (int s = 0; s < STAGES; ++s) mbar_init(&lo_full[s], 4 * CTAS);  // one per converter warp and CTA
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 1) {
@@ -382,18 +409,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 const int m0 = tm * BM * CTAS + (int)rank * BM, n0 = tn * BN + (int)rank * BNC;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if constexpr (CTAS == 1) {
+                    if constexpr (CTAS == 1 || PARTS == 2) {
                         mbar_expect_tx(&full[stage], STAGE_TX);
                     } else {
                         if (rank == 0) mbar_expect_tx(&full[stage], STAGE_TX);
                     }
+                    // TMA loads the raw tiles only (3xTF32: the lo parts are made in smem)
 #pragma unroll
-                    for (int part = 0; part < PARTS; ++part) {
+                    for (int part = 0; part < 1; ++part) {
                         uint8_t* a = sA + (stage * PARTS + part) * A_BYTES;
                         uint8_t* b = sB + (stage * PARTS + part) * B_BYTES;
                         const CUtensorMap* ma = part ? &mapAlo : &mapA;
                         const CUtensorMap* mb = part ? &mapBlo : &mapB;
-                        if constexpr (CTAS == 1) {
+                        if constexpr (CTAS == 1 || PARTS == 2) {  // this CTA's own barrier
                             if (!p.a_mn) {
                                 tma_load_2d(a, ma, &full[stage], kb * BK, m0);
                             } else {
@@ -457,7 +485,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                         tc_fence_after();
                         d = tmem_base + (uint32_t)acc * ACC_COLS;
                     }
-                    mbar_wait(&full[stage], phase);
+                    if constexpr (PARTS == 2) {
+                        mbar_wait(&lo_full[stage], phase);  // raw tiles landed and lo parts written, every CTA
+                    } else {
+                        mbar_wait(&full[stage], phase);
+                    }
                     tc_fence_after();
                     const uint32_t a0 = smem_addr(sA + stage * PARTS * A_BYTES);
                     const uint32_t b0 = smem_addr(sB + stage * PARTS * B_BYTES);
@@ -508,6 +540,53 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 if (++acc == ACC_STAGES) {
                     acc = 0;
                     acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (PARTS == 2 && warp >= 6) {  // ---- 3xTF32 converters: warps 6..9
+        // lo = x - hi(x) for every element of this CTA's raw A and B tiles,
+        // written at the same offset in the stage's lo part (the swizzle is a
+        // function of the offset, so the layout carries over), then released
+        // to the async proxy and counted on the leader's lo_full barrier
+        const int ct = threadIdx.x - 6 * 32;  // 0..127
+        int stage = 0;
+        uint32_t phase = 0;
+        const int iters = p.tiles_m * p.tiles_n;
+        for (int t = unit; t < iters; t += units) {
+            for (int kb = 0; kb < p.k_blocks; ++kb) {
+                mbar_wait(&full[stage], phase);
+                const uint4* ra = reinterpret_cast<const uint4*>(sA + stage * PARTS * A_BYTES);
+                uint4* la = reinterpret_cast<uint4*>(sA + stage * PARTS * A_BYTES + A_BYTES);
+#pragma unroll 4
+                for (int i = ct; i < (int)(A_BYTES / 16); i += 128) {
+                    const uint4 v = ra[i];
+                    la[i] = make_uint4(__float_as_uint(tf32_lo(__uint_as_float(v.x))),
+                                       __float_as_uint(tf32_lo(__uint_as_float(v.y))),
+                                       __float_as_uint(tf32_lo(__uint_as_float(v.z))),
+                                       __float_as_uint(tf32_lo(__uint_as_float(v.w))));
+                }
+                const uint4* rb = reinterpret_cast<const uint4*>(sB + stage * PARTS * B_BYTES);
+                uint4* lb = reinterpret_cast<uint4*>(sB + stage * PARTS * B_BYTES + B_BYTES);
+#pragma unroll 4
+                for (int i = ct; i < (int)(B_BYTES / 16); i += 128) {
+                    const uint4 v = rb[i];
+                    lb[i] = make_uint4(__float_as_uint(tf32_lo(__uint_as_float(v.x))),
+                                       __float_as_uint(tf32_lo(__uint_as_float(v.y))),
+                                       __float_as_uint(tf32_lo(__uint_as_float(v.z))),
+                                       __float_as_uint(tf32_lo(__uint_as_float(v.w))));
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tcgen05 reads
+                __syncwarp();
+                if (lane == 0) {
+                    if (rank == 0) {
+                        mbar_arrive(&lo_full[stage]);
+                    } else {
+                        mbar_arrive_remote(&lo_full[stage], 0);
+                    }
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
@@ -681,20 +760,7 @@ struct ConvertJobs {
     ConvertJob<D> j[4];
 };
 
-// 3xTF32 split: hi = the bits a tf32 MMA reads (low 13 mantissa bits
-// cleared), lo = x - hi, exact in fp32
-__host__ __device__ __forceinline__ float tf32_hi(float x) {
-#ifdef __CUDA_ARCH__
-    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-#else
-    uint32_t u;
-    std::memcpy(&u, &x, 4);
-    u &= 0xFFFFE000u;
-    std::memcpy(&x, &u, 4);
-    return x;
-#endif
-}
-__host__ __device__ __forceinline__ float tf32_lo(float x) { return x - tf32_hi(x); }
+
 
 // Both operands' staging in ONE launch: a flat grid-stride over the
 // (row, 4-column quad) space of job a then job b, 4 quads per thread per step
@@ -814,8 +880,9 @@ inline size_t staged_bytes(i64 rows, i64 cols) {
 }
 template <int KIND>
 inline size_t workspace_bytes(i64 M, i64 N, i64 K, int ta, int tb) {
+    // (3xTF32's lo parts are made in shared memory: its staging is tf32's)
     const OperandLayout a = layout_a(M, K, ta), b = layout_b(N, K, tb);
-    return (size_t)Elem<KIND>::PARTS * (staged_bytes<KIND>(a.rows, a.cols) + staged_bytes<KIND>(b.rows, b.cols));
+    return staged_bytes<KIND>(a.rows, a.cols) + staged_bytes<KIND>(b.rows, b.cols);
 }
 
 template <typename T>
@@ -873,21 +940,17 @@ int launch_tc(const GemmCall& c) {
         return tc_fail(c, AG_ERR_SHAPE, "problem too large for the tensor-core grid");
     const OperandLayout la = layout_a(M, K, c.ta), lb = layout_b(N, K, c.tb);
     const size_t need = workspace_bytes<KIND>(M, N, K, c.ta, c.tb);
-    if ((KIND == KIND_BF16 || Elem<KIND>::PARTS == 2) && (c.ws_bytes < need || c.ws == nullptr))
+    if (KIND == KIND_BF16 && (c.ws_bytes < need || c.ws == nullptr))
         return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
     const size_t a_st = staged_bytes<KIND>(la.rows, la.cols), b_st = staged_bytes<KIND>(lb.rows, lb.cols);
     char* wsA = static_cast<char*>(c.ws);
     char* wsB = wsA ? wsA + a_st : nullptr;
-    const void *baseA = nullptr, *baseB = nullptr, *baseAlo = nullptr, *baseBlo = nullptr;
-    i64 ldA = 0, ldB = 0, ldAlo = 0, ldBlo = 0;
+    (void)b_st;
+    const void *baseA = nullptr, *baseB = nullptr;
+    i64 ldA = 0, ldB = 0;
     ConvertJobs<T> jobs{};
     jobs.j[0] = plan_operand<KIND>(static_cast<const float*>(c.A), c.lda, la, wsA, &baseA, &ldA);
     jobs.j[1] = plan_operand<KIND>(static_cast<const float*>(c.B), c.ldb, lb, wsB, &baseB, &ldB);
-    if constexpr (Elem<KIND>::PARTS == 2) {  // 3xTF32: the lo parts always stage (hi is read in place when aligned)
-        jobs.j[2] = plan_operand<KIND>(static_cast<const float*>(c.A), c.lda, la, wsA + a_st + b_st, &baseAlo, &ldAlo, 1);
-        jobs.j[3] = plan_operand<KIND>(static_cast<const float*>(c.B), c.ldb, lb, wsA + 2 * a_st + b_st, &baseBlo,
-                                       &ldBlo, 1);
-    }
     const bool staged = jobs.j[0].quads || jobs.j[1].quads || jobs.j[2].quads || jobs.j[3].quads;
     if (staged && (c.ws_bytes < need || c.ws == nullptr))
         return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
@@ -896,18 +959,11 @@ int launch_tc(const GemmCall& c) {
     // A: K-major unless transA; B: MN-major unless transB.  Boxes are per
     // CTA: 128 rows of A, BN / CTAS rows of B.
     const int a_mn = c.ta ? 1 : 0, b_mn = c.tb ? 0 : 1;
-    CUtensorMap mapA, mapB, mapAlo, mapBlo;
+    CUtensorMap mapA, mapB;
     if (!make_map<KIND>(&mapA, baseA, la.rows, la.cols, ldA, a_mn, BM) ||
         !make_map<KIND>(&mapB, baseB, lb.rows, lb.cols, ldB, b_mn, BN / CTAS))
         return tc_fail(c, AG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    if constexpr (Elem<KIND>::PARTS == 2) {
-        if (!make_map<KIND>(&mapAlo, baseAlo, la.rows, la.cols, ldAlo, a_mn, BM) ||
-            !make_map<KIND>(&mapBlo, baseBlo, lb.rows, lb.cols, ldBlo, b_mn, BN / CTAS))
-            return tc_fail(c, AG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    } else {
-        mapAlo = mapA;
-        mapBlo = mapB;
-    }
+    const CUtensorMap &mapAlo = mapA, &mapBlo = mapB;  // (unused: the kernel's lo parts come from smem)
 
     TcParams p;
     p.M = (int)M;
@@ -941,7 +997,7 @@ int launch_tc(const GemmCall& c) {
     const i64 units = std::min<i64>(tiles_m * tiles_n, sm_count() / CTAS);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(units * CTAS));
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(kernel_threads<KIND>());
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[2];

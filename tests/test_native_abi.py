@@ -121,9 +121,11 @@ def test_tc_workspace_sizes():
     # each 1 KiB rounded
     want = -(-33 * 64 * 2 // 1024) * 1024 + -(-17 * 128 * 2 // 1024) * 1024
     assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(cfg.native()), 0) == want
-    # tf32x3: [A hi | B hi | A lo | B lo], fp32 rows rounded to 32 elements, each part 1 KiB rounded
+    # tf32x3 stages like tf32 (re-strided copies only for unaligned rows: fp32
+    # rows rounded to 32 elements, each 1 KiB rounded); its lo parts are made
+    # in shared memory
     x3 = KernelConfig(KernelFamily.TF32X3, 128, 128, 32, 2, 1, 1)
-    want3 = 2 * (-(-33 * 32 * 4 // 1024) * 1024 + -(-17 * 96 * 4 // 1024) * 1024)
+    want3 = -(-33 * 32 * 4 // 1024) * 1024 + -(-17 * 96 * 4 // 1024) * 1024
     assert lib.ag_workspace_bytes(ctypes.byref(s), ctypes.byref(x3.native()), 0) == want3
 
 
