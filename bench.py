@@ -304,7 +304,7 @@ def pack_launches(shape, cfg) -> int:
         return 1  # one clustered launch (skinny.cuh)
     if cfg.family in TC_FAMILIES:  # bf16: one convert pass per operand; tf32 reads fp32 in place
         if cfg.family is KernelFamily.TF32X3:
-            return 2  # one convert launch (both lo parts) + the tc kernel
+            return 1  # the lo parts are made in shared memory
         return 3 if cfg.family is KernelFamily.BF16 else 1
     if cfg.family is KernelFamily.TMA and not shape.transA and not shape.transB and shape.K % 4 == 0 \
             and shape.N % 4 == 0:
@@ -909,10 +909,10 @@ def x3_section(cases, default_t, device, distributed, times, fallback, args):
         traffic = json.loads(TRAFFIC_FILE.read_text()).get(key) if TRAFFIC_FILE.exists() else None
         roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32_peak / 3, 1), "unit": "TFLOP/s",
                 "frac": round(ach / (tf32_peak / 3), 4), "kernel": key, "traffic": traffic,
-                "traffic_note": "DRAM bytes of the tc_gemm launch alone (ncu --set full); the lo-part convert "
-                                "pass adds 8 B per operand element",
+                "traffic_note": "DRAM bytes of the tc_gemm launch (ncu --set full); the lo parts are made in "
+                                "shared memory, no other launch",
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 2 = tf32, / 3 products per K step",
-                "note": "event time covers the family path (lo-part convert pass included)"}
+                "note": "event time covers the family path (one launch)"}
     fams = {}
     for c in dt_cfgs:
         fams[c.family.value] = fams.get(c.family.value, 0) + 1

@@ -70,7 +70,7 @@ extern "C" {
 #define AG_FAMILY_SKINNY_M 7
 /* b200tc profile: fp32-accurate GEMM on the tensor pipe ("3xTF32").  Each
  * fp32 operand is split as x = hi + lo (hi = the bits a tf32 MMA reads,
- * lo = x - hi, staged by one convert pass); a.b ~ a_hi.b_hi + a_hi.b_lo +
+ * lo = x - hi, made in shared memory by converter warps); a.b ~ a_hi.b_hi + a_hi.b_lo +
  * a_lo.b_hi as three tcgen05 kind::tf32 MMAs per K step into one TMEM
  * accumulator.  Meets the fp32 families' RF <= 1e-5 contract.  Tile fields
  * as the tf32 family (bm 128 / 256, bn, bk = 32, tm = stages). */
