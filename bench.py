@@ -990,7 +990,9 @@ def sweep_section(device, distributed, rank, world, with_cpu):
     smoke config, test_acceptance.py:339-387), LPT-sharded shape-wise over the
     ranks with no collective (cli tune --gpus); wall time = max over ranks.
     Both the reference space (576 configs, what the CPU sweep times) and the
-    B200 profile; the reference's CPU sweep of the same shapes beside it."""
+    B200 profile, the latter also in the shipped labels' regime (L2 flushed
+    before every sample, 1 + 5); the reference's CPU sweep of the same
+    shapes beside it."""
     import torch
 
     from paper_1806_07060_b200 import distributed as dist_mod
@@ -1004,7 +1006,9 @@ def sweep_section(device, distributed, rank, world, with_cpu):
     out = {"shapes": len(shapes), "dataset": "po2(64, 256) (acceptance C11)", "ranks": world, "scaling": "strong",
            "timing": "warmup 1 + repeats 3 (warm)"}
     tune_exhaustive(ProblemShape(64, 64, 64), DeviceCaps.b200(), timing)  # warm every kernel once
-    for name, caps in (("reference_space", DeviceCaps()), ("b200_space", DeviceCaps.b200())):
+    flush = TimingPolicy(warmup=1, repeats=5, l2="flush")  # the shipped tables' label regime
+    for name, caps, timing in (("reference_space", DeviceCaps(), timing), ("b200_space", DeviceCaps.b200(), timing),
+                               ("b200_space_label_regime", DeviceCaps.b200(), flush)):
         n_cfg = len(full_search_space(caps))
         mine = dist_mod.shard(shapes, rank, world, lambda s: sweep_cost(s.mnk, n_cfg, 8))
         distributed.barrier()
@@ -1015,7 +1019,8 @@ def sweep_section(device, distributed, rank, world, with_cpu):
         torch.cuda.synchronize()
         wall = distributed.reduce_max([time.perf_counter() - t0], device)[0]
         flops = sum(2.0 * s.M * s.N * s.K for s in shapes) * n_cfg * (timing.warmup + timing.repeats)
-        out[name] = {"configs_per_shape": n_cfg, "configs_timed": n_cfg * len(shapes), "wall_s": round(wall, 3),
+        out[name] = {"timing": f"warmup {timing.warmup} + repeats {timing.repeats} ({timing.l2})",
+                     "configs_per_shape": n_cfg, "configs_timed": n_cfg * len(shapes), "wall_s": round(wall, 3),
                      "configs_per_s": round(n_cfg * len(shapes) / wall, 1),
                      "shapes_per_h": round(len(shapes) / wall * 3600, 1),
                      "swept_gflops_per_s": round(flops / wall / 1e9, 1)}

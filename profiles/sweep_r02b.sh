@@ -1,9 +1,10 @@
 #!/usr/bin/env bash
-# Round-2 re-sweep, resumable across gpurun calls: every label in bench.py's
-# timing regime (L2 flushed before every sample, trimmed mean of the samples).
-# Raw per-shape tables live in /tmp on the box; after each config (finished
-# or cut by its time limit) they are tarred into gpurun_out/sweep_tar/, and a
-# later call unpacks that tarball first so `tune` resumes where it stopped.
+# Round-2 re-sweep: every label in bench.py's timing regime (L2 flushed
+# before every sample, trimmed mean of the samples).  Raw per-shape tables
+# live in /tmp on the box; after each config (finished or cut by its time
+# limit) they are tarred into gpurun_out/sweep_tar/ and come back with the
+# call.  (gpurun does not ship gpurun_out/ to the box, so a cut sweep resumes
+# only if its tarball is copied into the repo tree before the next call.)
 #   gpurun --timeout 3000 -- 'LIMIT=2700 bash profiles/sweep_r02b.sh deepbench_b200 po2_b200'
 set -u
 O=gpurun_out
