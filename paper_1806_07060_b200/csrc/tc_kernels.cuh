@@ -300,8 +300,7 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) 
 // 128 output rows.  Per SM this halves the B traffic of a 128 x BN tile.
 template <int KIND, int BN, int STAGES, int CTAS>
 __global__ void __launch_bounds__(kernel_threads<KIND>(), 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-               const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo, TcParams p) {
+tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p) {
     constexpr int BK = Elem<KIND>::BK;
     constexpr int PARTS = Elem<KIND>::PARTS;  // [hi | lo] per operand and stage for 3xTF32
     constexpr int BNC = BN / CTAS;  // B rows (N) staged by each CTA
@@ -352,10 +351,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
-        if constexpr (PARTS == 2) {
-            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapAlo)) : "memory");
-            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapBlo)) : "memory");
-        }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -414,13 +409,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                     } else {
                         if (rank == 0) mbar_expect_tx(&full[stage], STAGE_TX);
                     }
-                    // TMA loads the raw tiles only (3xTF32: the lo parts are made in smem)
-#pragma unroll
-                    for (int part = 0; part < 1; ++part) {
-                        uint8_t* a = sA + (stage * PARTS + part) * A_BYTES;
-                        uint8_t* b = sB + (stage * PARTS + part) * B_BYTES;
-                        const CUtensorMap* ma = part ? &mapAlo : &mapA;
-                        const CUtensorMap* mb = part ? &mapBlo : &mapB;
+                    // TMA loads the raw tiles (3xTF32: its lo parts are made in smem)
+                    {
+                        uint8_t* a = sA + stage * PARTS * A_BYTES;
+                        uint8_t* b = sB + stage * PARTS * B_BYTES;
+                        const CUtensorMap* ma = &mapA;
+                        const CUtensorMap* mb = &mapB;
                         if constexpr (CTAS == 1 || PARTS == 2) {  // this CTA's own barrier
                             if (!p.a_mn) {
                                 tma_load_2d(a, ma, &full[stage], kb * BK, m0);
@@ -742,8 +736,7 @@ __device__ __forceinline__ void store4(__nv_bfloat16* d, float a, float b, float
 __device__ __forceinline__ void store1(float* d, float a) { *d = a; }
 __device__ __forceinline__ void store1(__nv_bfloat16* d, float a) { *d = __float2bfloat16_rn(a); }
 
-// One staging job: dst (rows x cols, ld_dst) = src converted to the MMA type,
-// or (lo = 1, fp32 only) the 3xTF32 low part x - hi(x).
+// One staging job: dst (rows x cols, ld_dst) = src converted to the MMA type.
 template <typename D>
 struct ConvertJob {
     D* dst;
@@ -752,7 +745,6 @@ struct ConvertJob {
     i64 ld_src;
     i64 rows, cols, quads;  // quads = rows * ceil(cols / 4); 0 = no job
     int vec;                // 16-byte source rows: one LDG.128 per quad
-    int lo;                 // write x - hi(x) (3xTF32 low part)
 };
 // every staging job of one call (up to hi / lo of A and B), one launch
 template <typename D>
@@ -780,12 +772,11 @@ __device__ __forceinline__ void convert_quad(const ConvertJob<D>& j, i64 q) {
         } else {
             v = make_float4(__ldcs(sp), __ldcs(sp + 1), __ldcs(sp + 2), __ldcs(sp + 3));
         }
-        if (j.lo) v = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
         store4(dp, v.x, v.y, v.z, v.w, true);
     } else {
         for (i64 k = c; k < j.cols; ++k) {
             const float x = j.src[r * j.ld_src + k];
-            store1(j.dst + r * j.ld_dst + k, j.lo ? tf32_lo(x) : x);
+            store1(j.dst + r * j.ld_dst + k, x);
         }
     }
 }
@@ -905,10 +896,10 @@ inline int tc_fail(const GemmCall& c, int code, const char* msg) {
 // conversion job (quads = 0 when the operand is read in place).
 template <int KIND>
 inline ConvertJob<typename Elem<KIND>::T> plan_operand(const float* src, i64 ld_src, OperandLayout lay, void* ws,
-                                                       const void** base, i64* ld, int lo = 0) {
+                                                       const void** base, i64* ld) {
     typedef typename Elem<KIND>::T T;
     ConvertJob<T> j{};
-    if (KIND != KIND_BF16 && !lo && ld_src % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+    if (KIND != KIND_BF16 && ld_src % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
         *base = src;
         *ld = ld_src;
         return j;
@@ -923,7 +914,6 @@ inline ConvertJob<typename Elem<KIND>::T> plan_operand(const float* src, i64 ld_
     j.cols = lay.cols;
     j.quads = lay.rows * ((lay.cols + 3) / 4);
     j.vec = (ld_src % 4 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0);
-    j.lo = lo;
     return j;
 }
 
@@ -942,10 +932,9 @@ int launch_tc(const GemmCall& c) {
     const size_t need = workspace_bytes<KIND>(M, N, K, c.ta, c.tb);
     if (KIND == KIND_BF16 && (c.ws_bytes < need || c.ws == nullptr))
         return tc_fail(c, AG_ERR_SHAPE, "workspace too small for the tensor-core staging buffers");
-    const size_t a_st = staged_bytes<KIND>(la.rows, la.cols), b_st = staged_bytes<KIND>(lb.rows, lb.cols);
+    const size_t a_st = staged_bytes<KIND>(la.rows, la.cols);
     char* wsA = static_cast<char*>(c.ws);
     char* wsB = wsA ? wsA + a_st : nullptr;
-    (void)b_st;
     const void *baseA = nullptr, *baseB = nullptr;
     i64 ldA = 0, ldB = 0;
     ConvertJobs<T> jobs{};
@@ -963,7 +952,6 @@ int launch_tc(const GemmCall& c) {
     if (!make_map<KIND>(&mapA, baseA, la.rows, la.cols, ldA, a_mn, BM) ||
         !make_map<KIND>(&mapB, baseB, lb.rows, lb.cols, ldB, b_mn, BN / CTAS))
         return tc_fail(c, AG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    const CUtensorMap &mapAlo = mapA, &mapBlo = mapB;  // (unused: the kernel's lo parts come from smem)
 
     TcParams p;
     p.M = (int)M;
@@ -1011,7 +999,7 @@ int launch_tc(const GemmCall& c) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = staged ? 2 : 1;
-    if (cudaLaunchKernelEx(&cfg, kernel, mapA, mapB, mapAlo, mapBlo, p) != cudaSuccess)
+    if (cudaLaunchKernelEx(&cfg, kernel, mapA, mapB, p) != cudaSuccess)
         return tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
     return cudaGetLastError() == cudaSuccess ? AG_OK : tc_fail(c, AG_ERR_CUDA, "tensor-core kernel launch failed");
 }
