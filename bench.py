@@ -727,7 +727,10 @@ def run_ours(args):
         "hybrid_model": {"model": hy["name"], "n_train": hy["n_train"], "n_test": hy["n_test"],
                          "note": "reference CLI hybrid dataset (po2 + DeepBench, one 80/20 split); DT measured "
                                  "live on the DeepBench shapes of each subset",
-                         "deepbench_train": hy_sub(hy["db_train"]), "deepbench_test": hy_sub(hy["db_test"])},
+                         "deepbench_train": hy_sub(hy["db_train"]), "deepbench_test": hy_sub(hy["db_test"]),
+                         "deepbench_all": dict(hy_sub([c.shape for c in cases]),
+                                               note="round 1's headline protocol (tree trained on po2 + 80 % "
+                                                    "of DeepBench), for comparison only")},
         "po2_test_split": {"shapes": len(po2_cases), "dataset": "po2 16..4096 (held-out 20 %)",
                            "dt_geomean": round(geomean(rate(po2_cases, po2_dt)), 2),
                            "oracle_geomean": round(geomean(rate(po2_cases, po2_or)), 2),
