@@ -610,6 +610,7 @@ struct HostCache {
     std::mutex mu;
     std::multimap<size_t, void*> free_blocks;  // size class -> block
     std::unordered_map<void*, size_t> sizes;   // every block this cache owns
+    std::unordered_map<void*, bool> cached_now;  // block -> sitting in free_blocks (a double free is ignored)
     size_t cached = 0, cap = (size_t)4 << 30;
     HostCache() {
         if (const char* e = std::getenv("AG_HOST_CACHE_BYTES")) cap = (size_t)std::strtoull(e, nullptr, 10);
@@ -633,6 +634,7 @@ void* ag_host_alloc(size_t bytes) {
             void* p = it->second;
             hc.cached -= it->first;
             hc.free_blocks.erase(it);
+            hc.cached_now[p] = false;
             return p;
         }
     }
@@ -643,6 +645,7 @@ void* ag_host_alloc(size_t bytes) {
     }
     std::lock_guard<std::mutex> lk(hc.mu);
     hc.sizes[p] = sz;
+    hc.cached_now[p] = false;
     return p;
 }
 
@@ -651,14 +654,16 @@ void ag_host_free(void* p) {
     HostCache& hc = host_cache();
     std::lock_guard<std::mutex> lk(hc.mu);
     auto s = hc.sizes.find(p);
-    if (s == hc.sizes.end()) return;
+    if (s == hc.sizes.end() || hc.cached_now[p]) return;  // not ours, or already freed
     hc.free_blocks.emplace(s->second, p);
+    hc.cached_now[p] = true;
     hc.cached += s->second;
     while (hc.cached > hc.cap && !hc.free_blocks.empty()) {  // drop the largest cached blocks first
         auto last = std::prev(hc.free_blocks.end());
         cudaFreeHost(last->second);
         hc.cached -= last->first;
         hc.sizes.erase(last->second);
+        hc.cached_now.erase(last->second);
         hc.free_blocks.erase(last);
     }
 }
@@ -866,21 +871,25 @@ int ag_gemm_host_ex(const ag_shape* s, const ag_config* c, const ag_caps* caps, 
     int launched = 0;  // panels whose family path is enqueued (-1: abort)
     cudaError_t drain_err = cudaSuccess;
     std::thread drainer;
-    const bool drain_thread = !pin_o && h.panels > 1;
+    bool drain_thread = !pin_o && h.panels > 1;
     if (drain_thread) {
         int dev_id = 0;
         cudaGetDevice(&dev_id);
-        drainer = std::thread([&, dev_id] {
-            cudaSetDevice(dev_id);  // the current device is per host thread
-            for (int p = 0; p < h.panels; ++p) {
-                {
-                    std::unique_lock<std::mutex> lk(dm);
-                    dcv.wait(lk, [&] { return launched > p || launched < 0; });
-                    if (launched < 0) return;
+        try {
+            drainer = std::thread([&, dev_id] {
+                cudaSetDevice(dev_id);  // the current device is per host thread
+                for (int p = 0; p < h.panels; ++p) {
+                    {
+                        std::unique_lock<std::mutex> lk(dm);
+                        dcv.wait(lk, [&] { return launched > p || launched < 0; });
+                        if (launched < 0) return;
+                    }
+                    drain(p, drain_err);
                 }
-                drain(p, drain_err);
-            }
-        });
+            });
+        } catch (const std::exception&) {  // no thread: drain on this one, panel by panel
+            drain_thread = false;
+        }
     }
     auto publish = [&](int n) {
         if (!drain_thread) return;

@@ -409,3 +409,20 @@ def test_pinned_result_blocks_are_cached_and_exact():
     assert _native.lib().ag_host_cache_bytes() == fp.cache_bytes()
     small, _ = gemm_execute(ProblemShape(64, 64, 64), cfg, *rand_operands(ProblemShape(64, 64, 64), seed=4))
     assert small.base is None  # under 1 MB: np.empty
+
+
+def test_host_alloc_double_free_is_ignored():
+    """ag_host_free on a block twice must not cache it twice (two later
+    allocations would then share it); foreign pointers are ignored."""
+    from paper_1806_07060_b200 import _native
+    L = _native.lib()
+    n = 3 << 20
+    p = L.ag_host_alloc(n)
+    assert p
+    L.ag_host_free(p)
+    L.ag_host_free(p)
+    L.ag_host_free(12345)  # not a block of the cache
+    a, b = L.ag_host_alloc(n), L.ag_host_alloc(n)
+    assert a and b and a != b
+    L.ag_host_free(a)
+    L.ag_host_free(b)
