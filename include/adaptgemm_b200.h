@@ -179,9 +179,10 @@ void* ag_device_scratch(size_t bytes);
 
 /* Caching pinned host allocator for host-path RESULTS (the fresh numpy
  * output of gemm_execute(..., out=None), kernels.py:328-349): page-locked
- * (cudaHostAllocPortable) blocks in 2 MB size classes, reused after
- * ag_host_free, at most AG_HOST_CACHE_BYTES (env, default 4 GiB) kept
- * cached.  A result written into such a block arrives by DMA with no
+ * (cudaHostAllocPortable) blocks in power-of-two size classes from 64 KB
+ * to 2 MB and 2 MB multiples above, reused after ag_host_free, at most
+ * AG_HOST_CACHE_BYTES (env, default 4 GiB) kept cached and at most
+ * AG_HOST_PINNED_MAX_BYTES (default 16 GiB) owned in all.  A result written into such a block arrives by DMA with no
  * staging copy and no first-touch page faults.  NULL when pinning fails
  * (the caller then allocates pageable memory). */
 void* ag_host_alloc(size_t bytes);

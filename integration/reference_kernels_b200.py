@@ -119,7 +119,7 @@ def _pinned_result(L, m, n, dtype):
     block goes back to the cache when the array is collected.  Small results
     (or a failed pin) are plain np.empty."""
     nbytes = m * n * np.dtype(dtype).itemsize
-    p = L.ag_host_alloc(nbytes) if nbytes >= (1 << 20) else None
+    p = L.ag_host_alloc(nbytes) if nbytes >= (64 << 10) else None
     if not p:
         return np.empty((m, n), dtype=dtype)
     raw = (ctypes.c_char * nbytes).from_address(p)

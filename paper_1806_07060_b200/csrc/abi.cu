@@ -611,9 +611,11 @@ struct HostCache {
     std::multimap<size_t, void*> free_blocks;  // size class -> block
     std::unordered_map<void*, size_t> sizes;   // every block this cache owns
     std::unordered_map<void*, bool> cached_now;  // block -> sitting in free_blocks (a double free is ignored)
-    size_t cached = 0, cap = (size_t)4 << 30;
+    size_t cached = 0, cap = (size_t)4 << 30;  // free blocks kept
+    size_t owned = 0, owned_cap = (size_t)16 << 30;  // every block (live + cached): beyond it, callers go pageable
     HostCache() {
         if (const char* e = std::getenv("AG_HOST_CACHE_BYTES")) cap = (size_t)std::strtoull(e, nullptr, 10);
+        if (const char* e = std::getenv("AG_HOST_PINNED_MAX_BYTES")) owned_cap = (size_t)std::strtoull(e, nullptr, 10);
     }
 };
 HostCache& host_cache() {
@@ -624,8 +626,11 @@ HostCache& host_cache() {
 
 void* ag_host_alloc(size_t bytes) {
     if (!bytes) return nullptr;
+    // size classes: powers of two from 64 KB up to 2 MB, then 2 MB multiples
     constexpr size_t kClass = 2u << 20;
-    const size_t sz = (bytes + kClass - 1) / kClass * kClass;
+    size_t sz = (size_t)64 << 10;
+    while (sz < bytes && sz < kClass) sz <<= 1;
+    if (bytes > kClass) sz = (bytes + kClass - 1) / kClass * kClass;
     HostCache& hc = host_cache();
     {
         std::lock_guard<std::mutex> lk(hc.mu);
@@ -638,6 +643,10 @@ void* ag_host_alloc(size_t bytes) {
             return p;
         }
     }
+    {
+        std::lock_guard<std::mutex> lk(hc.mu);
+        if (hc.owned + sz > hc.owned_cap) return nullptr;  // too much pinned memory alive: the caller goes pageable
+    }
     void* p = nullptr;
     if (cudaHostAlloc(&p, sz, cudaHostAllocPortable) != cudaSuccess) {
         cudaGetLastError();
@@ -646,6 +655,7 @@ void* ag_host_alloc(size_t bytes) {
     std::lock_guard<std::mutex> lk(hc.mu);
     hc.sizes[p] = sz;
     hc.cached_now[p] = false;
+    hc.owned += sz;
     return p;
 }
 
@@ -662,6 +672,7 @@ void ag_host_free(void* p) {
         auto last = std::prev(hc.free_blocks.end());
         cudaFreeHost(last->second);
         hc.cached -= last->first;
+        hc.owned -= last->first;
         hc.sizes.erase(last->second);
         hc.cached_now.erase(last->second);
         hc.free_blocks.erase(last);

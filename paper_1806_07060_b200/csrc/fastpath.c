@@ -7,7 +7,7 @@
  * -> ag_gemm_host_ex (H2D, family path, D2H in one blocking call; pageable
  * operands staged through the library's pinned rings, AG_HOST_STAGE; the
  * library's own device scratch) with the GIL released -> (out, device
- * seconds of the family path).  A fresh result (out=None) of 1 MB or more is
+ * seconds of the family path).  A fresh result (out=None) of 64 KB or more is
  * a numpy array over a block of the library's caching pinned allocator.
  *
  * Operands that are not plain row-major float32/float64 numpy arrays make
@@ -116,7 +116,7 @@ static PyTypeObject PinnedBlockType = {
     .tp_doc = "page-locked result block (ag_host_alloc)",
 };
 
-#define PINNED_OUT_MIN (1 << 20) /* smaller results: np.empty (a pageable copy costs less than a block) */
+#define PINNED_OUT_MIN (64 << 10) /* smaller results: np.empty (the small-call path stages them anyway) */
 
 /* a fresh m x n result: pinned when large enough and the cache can pin it,
  * else np.empty */

@@ -376,7 +376,7 @@ def test_staged_host_path_multi_panel_bit_exact(mnk, name):
 
 
 def test_pinned_result_blocks_are_cached_and_exact():
-    """A fresh result of >= 1 MB lives in a block of the library's caching
+    """A fresh result of >= 64 KB lives in a block of the library's caching
     pinned allocator (ag_host_alloc): a plain, writable numpy array with the
     device path's bits; dropping it returns the block to the cache and the
     next call of that size reuses it."""
@@ -408,7 +408,7 @@ def test_pinned_result_blocks_are_cached_and_exact():
     np.testing.assert_array_equal(again, ref.cpu().numpy())
     assert _native.lib().ag_host_cache_bytes() == fp.cache_bytes()
     small, _ = gemm_execute(ProblemShape(64, 64, 64), cfg, *rand_operands(ProblemShape(64, 64, 64), seed=4))
-    assert small.base is None  # under 1 MB: np.empty
+    assert small.base is None  # under 64 KB: np.empty
 
 
 def test_host_alloc_double_free_is_ignored():
