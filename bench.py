@@ -759,6 +759,13 @@ def run_ours(args):
                 "per_shape_ms": [[list(c.shape.mnk), round(t * 1e3, 3), round(u * 1e3, 3)]
                                  for c, t, u in zip(cases, e2e_t, pinned_t)],
                 "per_shape_columns": ["mnk", "numpy_dispatch_and_run_ms", "pinned_dispatch_native_ms"]},
+        "regime_floor": {
+            "note": "per shape, max(2MNK at the measured FFMA peak, the bench regime's streaming-read floor for "
+                    "its operand + result bytes, profiles/r02_read_floor.jsonl); geomean of floor / measured time",
+            "dt_frac": round(geomean(regime_floor_s(c.shape, peak_meas) / t for c, t in zip(cases, dt_t)), 4),
+            "oracle_frac": round(geomean(regime_floor_s(c.shape, peak_meas) / t for c, t in zip(cases, oracle_t)), 4),
+            "per_shape_dt_frac": [[list(c.shape.mnk), round(regime_floor_s(c.shape, peak_meas) / t, 3)]
+                                  for c, t in zip(cases, dt_t)]},
         "roofline": {"bound": "fp32-cuda-core (compute)", "achieved": round(achieved, 3),
                      "peak": round(peak_meas, 3), "unit": "TFLOP/s", "frac": round(achieved / peak_meas, 4),
                      "traffic": traffic, "kernel": key,
@@ -859,6 +866,31 @@ def load_x3_tables():
         return [merge_tables(t, by[t.shape.mnk]) for t in load_table_bundle(base)]
 
     return merged(PO2_BUNDLE, X3_PO2_BUNDLE), merged(DB_BUNDLE, X3_DB_BUNDLE)
+
+
+# The bench regime's streaming-read floor (profiles/r02_read_floor.jsonl,
+# profiles/read_floor.py): event time of a plain chunked read kernel of N MB
+# after the 256 MB write flush, best over grid sizes and unroll depths.
+READ_FLOOR_US = ((0.25, 6.18), (1, 6.18), (4, 8.19), (8, 8.19), (17, 10.24), (34, 14.34), (52, 18.43),
+                 (70, 22.53), (87, 24.61), (120, 31.74))
+
+
+def regime_floor_s(shape, ffma_tflops):
+    """The fastest any kernel could be in the bench regime: the FFMA time of
+    2MNK at the measured peak, or the time to merely read the operands and
+    write the result (interpolated read floor), whichever is longer."""
+    mb = 4.0 * (shape.M * shape.K + shape.K * shape.N + shape.M * shape.N) / (1 << 20)
+    pts = READ_FLOOR_US
+    if mb <= pts[0][0]:
+        us = pts[0][1]
+    elif mb >= pts[-1][0]:
+        us = pts[-1][1] + (mb - pts[-1][0]) * (pts[-1][1] - pts[-2][1]) / (pts[-1][0] - pts[-2][0])
+    else:
+        for (m0, t0), (m1, t1) in zip(pts, pts[1:]):
+            if m0 <= mb <= m1:
+                us = t0 + (mb - m0) * (t1 - t0) / (m1 - m0)
+                break
+    return max(2.0 * shape.M * shape.N * shape.K / (ffma_tflops * 1e12), us * 1e-6)
 
 
 def x3_section(cases, default_t, device, distributed, times, fallback, args):
