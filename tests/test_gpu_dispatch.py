@@ -426,3 +426,35 @@ def test_host_alloc_double_free_is_ignored():
     assert a and b and a != b
     L.ag_host_free(a)
     L.ag_host_free(b)
+
+
+def test_staged_host_path_concurrent_callers():
+    """Two host threads in the staged numpy path at once (the fast path
+    releases the GIL): per-thread pipes and rings, the shared copy pool and
+    the pinned result cache; every result equals its device-path bits."""
+    import threading
+
+    import torch
+    cfg = KernelConfig.from_canonical("indirect:64-64-32-8-8-1")
+    shapes = [ProblemShape(1500, 900, 700), ProblemShape(900, 1500, 600, beta=0.5)]
+    data = [rand_operands(s, seed=i + 7) for i, s in enumerate(shapes)]
+    caps = DeviceCaps.b200()
+    refs = [gemm_execute(s, cfg, *(torch.from_numpy(x).cuda() for x in d), caps)[0].cpu().numpy()
+            for s, d in zip(shapes, data)]
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(6):
+                out, _ = gemm_execute(shapes[i], cfg, *data[i], caps)
+                if not np.array_equal(out, refs[i]):
+                    errors.append(f"thread {i}: mismatch")
+        except Exception as exc:  # noqa: BLE001
+            errors.append(f"thread {i}: {exc!r}")
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
