@@ -10,7 +10,7 @@
 using namespace ag;
 
 struct Exp { int kind, a, b, c; LaunchFn fn; };  // kind 0: skinny_n<TM,BN,NW>, 1: skinny_m<BM,TN2,NW>
-#define N_LIST(X) X(1, 16, 4) X(1, 16, 8) X(2, 16, 4) X(2, 16, 8) X(4, 16, 4) X(1, 32, 4) X(1, 32, 8) X(2, 32, 4) X(2, 32, 8) X(1, 64, 4) X(1, 64, 8)
+#define N_LIST(X) X(1, 16, 4) X(1, 16, 8) X(2, 16, 4) X(2, 16, 8) X(4, 16, 4) X(1, 32, 4) X(1, 32, 8) X(2, 32, 4) X(2, 32, 8) X(1, 64, 4) X(1, 64, 8) X(4, 32, 4) X(2, 64, 4)
 #define M_LIST(X) X(40, 2, 4) X(40, 2, 8) X(48, 2, 4) X(24, 2, 4) X(16, 4, 4) X(32, 2, 4) X(16, 2, 4) X(8, 4, 4)
 // kind 2: skinny_m<40, 2, NW> with the B granule ring varied: (QK k per granule, NBUF buffers)
 #define M2_LIST(X) X(8, 4, 4) X(4, 4, 4) X(4, 8, 4) X(8, 2, 8) X(8, 4, 8) X(4, 8, 8)

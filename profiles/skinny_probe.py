@@ -56,7 +56,13 @@ def main():
     ws = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
     only = os.environ.get("SHAPES")
-    for (m, nn, k), base in BASE.items():
+    base_items = dict(BASE)
+    if only == "midn":  # N = 64 / 128 shapes (the skinny_n DT picks), round-2 picks as the base
+        base_items = {(1760, 64, 1760): "skinny_n:64-16-32-2-8-1", (2048, 64, 2048): "skinny_n:64-16-32-2-8-1",
+                      (2560, 64, 2560): "skinny_n:64-16-32-2-8-1", (1760, 128, 1760): "skinny_n:64-32-32-2-8-1",
+                      (2048, 128, 2048): "skinny_n:64-32-32-2-8-1", (4096, 64, 4096): "skinny_n:64-32-32-2-8-1",
+                      (3072, 64, 1024): "skinny_n:64-16-32-2-8-1", (7680, 64, 2560): "skinny_n:64-32-32-2-8-1"}
+    for (m, nn, k), base in base_items.items():
         if only == "m35" and m != 35:
             continue
         a = torch.rand(m, k, device="cuda") - 0.5
@@ -84,7 +90,7 @@ def main():
         res["base " + base] = [round(ts[10] * 1e6, 2), round(flops / ts[10] / 1e12, 2)]
         best = None
         for i, (kind, p1, p2, p3) in enumerate(infos):
-            if (kind == 0 and nn > 64) or (kind in (1, 2) and m > 64):
+            if (kind == 0 and nn > 128) or (kind in (1, 2) and m > 64):
                 continue
             if kind == 2 and m != 35:
                 continue
