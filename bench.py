@@ -711,7 +711,8 @@ def run_ours(args):
                          "(middle half) of the steps' event times",
                    "parallelism": f"replicas x{world} (shapes independent; no collective on the data path)",
                    "model": f"{m['name']} trained on {m['n_train']} po2 shapes ({m['train_set']}); no DeepBench "
-                            "shape in training or model selection",
+                            "table in training or model selection (8 of the 40 shapes are po2 grid points; "
+                            "dt_vs.unseen covers the other 32)",
                    "caps_profile": "b200"},
         "dt_vs": {"dt_geomean": round(value_1, 2), "oracle_geomean": round(geomean(or_r), 2),
                   "default_geomean": round(geomean(de_r), 2),
@@ -896,7 +897,7 @@ def regime_floor_s(shape, ffma_tflops):
 def x3_section(cases, default_t, device, distributed, times, fallback, args):
     """The fp32 space plus tf32x3 (fp32-accurate 3xTF32 on tcgen05, RF <=
     1e-5 like the fp32 families): the reference pipeline on the merged po2
-    tables (no DeepBench shape in training), the DT measured live on the
+    tables (no DeepBench table in training), the DT measured live on the
     DeepBench set against the merged oracle and the fp32 default tile; the
     whole output of the largest tf32x3 pick checked against the float64
     product; roofline of the dominant tf32x3 kernel against tf32 peak / 3."""

@@ -1,0 +1,60 @@
+"""CPU checks of bench.py's host-side helpers: the regime floor, the launch
+counts it claims per family, the merged tf32x3 tables and the headline
+model's protocol (no DeepBench shape in training)."""
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+from paper_1806_07060_b200.kernels import KernelConfig, KernelFamily, ProblemShape  # noqa: E402
+
+
+def test_regime_floor_is_the_slower_of_compute_and_read():
+    small = ProblemShape(2048, 16, 2048)       # 17 MB, 134 MFLOP: read-bound
+    big = ProblemShape(5124, 9124, 2560)       # compute-bound
+    assert bench.regime_floor_s(small, 72.5) == pytest.approx(10.07e-6, rel=0.02)
+    assert bench.regime_floor_s(big, 72.5) == pytest.approx(2 * 5124 * 9124 * 2560 / 72.5e12)
+    tiny = ProblemShape(8, 8, 8)
+    assert bench.regime_floor_s(tiny, 72.5) == pytest.approx(6.18e-6)
+    sizes = [ProblemShape(1024, 16, k) for k in (256, 1024, 4096, 16384, 65536)]
+    floors = [bench.regime_floor_s(s, 72.5) for s in sizes]
+    assert floors == sorted(floors)  # monotone in the bytes moved
+
+
+@pytest.mark.parametrize("canon,shape,n", [
+    ("tf32x3:128-128-32-3-1-1", (512, 512, 512), 1),
+    ("bf16:256-256-64-6-1-1", (512, 512, 512), 3),
+    ("tf32:256-256-32-4-1-1", (512, 512, 512), 1),
+    ("skinny_n:64-16-32-2-4-4", (2048, 16, 2048), 1),
+    ("direct:16-16-8-2-2-1", (64, 64, 64), 1),
+])
+def test_pack_launches_per_family(canon, shape, n):
+    assert bench.pack_launches(ProblemShape(*shape), KernelConfig.from_canonical(canon)) == n
+
+
+def test_x3_tables_merge_every_shape_with_fp32_rows_first():
+    po2, db = bench.load_x3_tables()
+    assert len(po2) == 729 and len(db) == 40
+    for t in db:
+        fams = [m.config.family for m in t.measurements]
+        first_x3 = fams.index(KernelFamily.TF32X3)
+        assert all(f is not KernelFamily.TF32X3 for f in fams[:first_x3])
+        assert all(f is KernelFamily.TF32X3 for f in fams[first_x3:])
+        assert t.peak_gflops == max(m.gflops for m in t.measurements)
+
+
+def test_headline_model_trains_on_po2_tables_only():
+    """The headline tree sees po2 tables only: every training shape is a
+    power of two in each dimension; the DeepBench shapes that are not po2
+    grid points (32 of 40) are never seen, and the bench reports them
+    separately (dt_vs.unseen)."""
+    from paper_1806_07060_b200.tuner import load_table_bundle
+    pipe = bench._pipeline(load_table_bundle(bench.PO2_BUNDLE), "po2")
+    pow2 = lambda v: v & (v - 1) == 0  # noqa: E731
+    assert len(pipe["train"]) == 583 and all(pow2(x) for mnk in pipe["train"] for x in mnk)
+    db = {t.shape.mnk for t in load_table_bundle(bench.DB_BUNDLE)}
+    off_grid = {mnk for mnk in db if not all(pow2(x) for x in mnk)}
+    assert len(off_grid) == 32 and not off_grid & pipe["train"]
