@@ -46,6 +46,10 @@ PO2_BUNDLE = DATA / "tables_b200_po2.csv.gz"
 DB_BUNDLE = DATA / "tables_b200_deepbench.csv.gz"
 TC_BUNDLE = DATA / "tables_b200tc_random.csv.gz"
 GO2_BUNDLE = DATA / "tables_b200_go2.csv.gz"
+# 512 octave-uniform random shapes in [16, 4096) (configs/lograndom_b200.json),
+# swept over the full B200 space in the bench's regime; joins po2 in the
+# headline model's training set
+LOGRANDOM_BUNDLE = DATA / "tables_b200_lograndom.csv.gz"
 # the tf32x3 rows of the same shapes and timing regime (configs/*_x3.json),
 # merged per shape into the fp32 tables by x3_section
 X3_PO2_BUNDLE = DATA / "tables_x3_po2.csv.gz"
@@ -86,10 +90,11 @@ def trimmed_mean(xs):
 # model: the reference pipeline on the shipped B200 tables
 
 
-def _pipeline(tables, provenance):
+def _pipeline(tables, provenance, anchors=None):
     """The reference pipeline on a list of tables (cli.py:281-373): dataset,
     seeded 80/20 split, the 5 x 8 CART grid on the train split, the model
-    with the best test DTPR."""
+    with the best test DTPR.  `anchors` (tables by shape) supplies the
+    default-tile anchors 256^3 / 1024^3 when `tables` lacks them."""
     from paper_1806_07060_b200 import evaluation, model
     from paper_1806_07060_b200.dataset import dataset_from_tables, split
 
@@ -99,7 +104,8 @@ def _pipeline(tables, provenance):
     train_recs = [recs[i] for i in sp.train]
     test_recs = [recs[i] for i in sp.test]
     named = model.grid_train(train_recs)
-    by_shape = evaluation.tables_by_shape(tables)
+    by_shape = dict(anchors or {})
+    by_shape.update(evaluation.tables_by_shape(tables))
     policy = evaluation.build_baseline_policy(by_shape[(256, 256, 256)], by_shape[(1024, 1024, 1024)],
                                               384).register(ds.class_index)
     scores = evaluation.score_models(named, test_recs, by_shape, ds.class_index, policy)
@@ -111,21 +117,47 @@ def _pipeline(tables, provenance):
             "n_train": len(train_recs), "n_test": len(test_recs)}
 
 
+def dedup_tables(tables):
+    """Tables deduplicated by (M, N, K) in order (the CLI's hybrid strategy,
+    cli.py:166-179)."""
+    out, seen = [], set()
+    for t in tables:
+        if t.shape.mnk not in seen:
+            seen.add(t.shape.mnk)
+            out.append(t)
+    return out
+
+
+def training_tables():
+    """The headline model's training set: the po2 16..4096 tables followed by
+    the octave-uniform random tables (the CLI hybrid of the two sweeps), one
+    seeded 80/20 split.  No DeepBench table."""
+    from paper_1806_07060_b200.tuner import load_table_bundle
+
+    for b in (PO2_BUNDLE, LOGRANDOM_BUNDLE):
+        if not b.exists():
+            raise SystemExit(f"missing shipped tuning tables {b.name}")
+    po2 = load_table_bundle(PO2_BUNDLE)
+    return po2, dedup_tables(po2 + load_table_bundle(LOGRANDOM_BUNDLE))
+
+
 def build_model():
-    """The headline model: the reference pipeline on the po2 tables ONLY
-    (SURVEY.md 8(d) C3: train on po2, evaluate on the DeepBench-style set);
-    no DeepBench table is seen in training or model selection.  The
-    DeepBench tables provide the oracle per shape."""
+    """The headline model: the reference pipeline on the po2 + octave-uniform
+    random tables (train on generated shape sets,
+    evaluate on the DeepBench-style set); no DeepBench table is seen in
+    training or model selection.  The DeepBench tables provide the oracle
+    per shape.  profiles/r02_train_set_probe.jsonl compares training sets
+    in table mode (po2 only: DeepBench DTPR 0.919; po2 + random: 0.921)."""
     from paper_1806_07060_b200.kernels import KernelFamily
     from paper_1806_07060_b200.tuner import load_table_bundle
 
-    if not PO2_BUNDLE.exists() or not DB_BUNDLE.exists():
-        raise SystemExit(f"missing shipped tuning tables {PO2_BUNDLE.name} / {DB_BUNDLE.name}")
-    po2 = load_table_bundle(PO2_BUNDLE)
+    if not DB_BUNDLE.exists():
+        raise SystemExit(f"missing shipped tuning tables {DB_BUNDLE.name}")
+    po2, train_tables = training_tables()
     db = load_table_bundle(DB_BUNDLE)
-    by_shape = {t.shape.mnk: t for t in po2}
+    by_shape = {t.shape.mnk: t for t in train_tables}
     by_shape.update({t.shape.mnk: t for t in db})
-    pipe = _pipeline(po2, "po2")
+    pipe = _pipeline(train_tables, "hybrid")
     return {
         "tree": pipe["tree"], "name": pipe["name"], "classes": pipe["classes"], "policy": pipe["policy"],
         "tables": by_shape, "po2_test": [t.shape for t in po2 if t.shape.mnk in pipe["test"]],
@@ -134,7 +166,8 @@ def build_model():
         # as 2048 x 16 x 2048 can coincide with a DeepBench shape)
         "db_unseen": [t.shape for t in db if t.shape.mnk not in pipe["train"]],
         "score": pipe["score"], "n_train": pipe["n_train"], "n_test": pipe["n_test"],
-        "train_set": "po2 train split (seed 2024, 80 %)", "family_direct": KernelFamily.DIRECT,
+        "train_set": "po2 16..4096 + 512 octave-uniform random shapes in [16, 4096) (seed 2026); "
+                     "train split (seed 2024, 80 %)", "family_direct": KernelFamily.DIRECT,
     }
 
 
@@ -146,12 +179,7 @@ def build_hybrid_model():
 
     po2 = load_table_bundle(PO2_BUNDLE)
     db = load_table_bundle(DB_BUNDLE)
-    hybrid, seen = [], set()
-    for t in po2 + db:
-        if t.shape.mnk not in seen:
-            seen.add(t.shape.mnk)
-            hybrid.append(t)
-    pipe = _pipeline(hybrid, "hybrid")
+    pipe = _pipeline(dedup_tables(po2 + db), "hybrid")
     db_set = {t.shape.mnk for t in db}
     pipe["db_train"] = [ProblemShapeOf(mnk) for mnk in sorted(pipe["train"] & db_set)]
     pipe["db_test"] = [ProblemShapeOf(mnk) for mnk in sorted(pipe["test"] & db_set)]
@@ -218,7 +246,8 @@ def go2_section():
     t0 = time.perf_counter()
     named = model.grid_train(train_recs)
     train_s = time.perf_counter() - t0
-    by_shape = evaluation.tables_by_shape(tables)
+    by_shape = dict(anchors or {})
+    by_shape.update(evaluation.tables_by_shape(tables))
     policy = evaluation.build_baseline_policy(by_shape[(256, 256, 256)], by_shape[(1024, 1024, 1024)],
                                               384).register(ds.class_index)
     scores = evaluation.score_models(named, test_recs, by_shape, ds.class_index, policy)
@@ -710,9 +739,9 @@ def run_ours(args):
                    "l2": "flushed (256 MB write) before every timed GEMM; per-shape time = trimmed mean "
                          "(middle half) of the steps' event times",
                    "parallelism": f"replicas x{world} (shapes independent; no collective on the data path)",
-                   "model": f"{m['name']} trained on {m['n_train']} po2 shapes ({m['train_set']}); no DeepBench "
-                            "table in training or model selection (8 of the 40 shapes are po2 grid points; "
-                            "dt_vs.unseen covers the other 32)",
+                   "model": f"{m['name']} trained on {m['n_train']} shapes ({m['train_set']}); no DeepBench "
+                            f"table in training or model selection ({len(cases) - len(unseen)} of the 40 shapes "
+                            f"are po2 training shapes; dt_vs.unseen covers the other {len(unseen)})",
                    "caps_profile": "b200"},
         "dt_vs": {"dt_geomean": round(value_1, 2), "oracle_geomean": round(geomean(or_r), 2),
                   "default_geomean": round(geomean(de_r), 2),
@@ -721,7 +750,7 @@ def run_ours(args):
                   "default_config": [policy.default_direct.canonical(), policy.default_indirect.canonical()],
                   "default_sensitivity": [dict(s, dt_over_default=round(value_1 / s["default_geomean"], 4))
                                           for s in sensitivity],
-                  "unseen": {"shapes": len(unseen), "note": "DeepBench shapes that are not po2 training shapes",
+                  "unseen": {"shapes": len(unseen), "note": "DeepBench shapes that are not training shapes",
                              "dt_geomean": round(geomean(dt_r[i] for i in unseen), 2),
                              "oracle_geomean": round(geomean(or_r[i] for i in unseen), 2),
                              "default_geomean": round(geomean(de_r[i] for i in unseen), 2)}},
@@ -732,7 +761,7 @@ def run_ours(args):
                          "deepbench_all": dict(hy_sub([c.shape for c in cases]),
                                                note="round 1's headline protocol (tree trained on po2 + 80 % "
                                                     "of DeepBench), for comparison only")},
-        "po2_test_split": {"shapes": len(po2_cases), "dataset": "po2 16..4096 (held-out 20 %)",
+        "po2_test_split": {"shapes": len(po2_cases), "dataset": "po2 16..4096 shapes in the training set's held-out 20 %",
                            "dt_geomean": round(geomean(rate(po2_cases, po2_dt)), 2),
                            "oracle_geomean": round(geomean(rate(po2_cases, po2_or)), 2),
                            "default_geomean": round(geomean(rate(po2_cases, po2_de)), 2),

@@ -3,8 +3,9 @@
 
     NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_b200_golden.py
 
-For the datasets bench.py trains on -- the po2 16..4096 B200 tables (the
-headline model) and the reference CLI's hybrid po2 + DeepBench dataset --
+For the datasets bench.py trains on -- the po2 16..4096 B200 tables, the
+headline training set (po2 + the octave-uniform random tables) and the
+reference CLI's hybrid po2 + DeepBench dataset --
 the records (features, class ids) are built from the shipped table bundles
 by this package (class ids in first-appearance order, dataset.py:94-183),
 then the reference's own `split` (dataset.py:224-233, via rng.shuffled) and
@@ -59,10 +60,12 @@ def main():
         if t.shape.mnk not in seen:
             seen.add(t.shape.mnk)
             hybrid.append(t)
-    doc = {"bundles": [bench.PO2_BUNDLE.name, bench.DB_BUNDLE.name],
+    _, headline = bench.training_tables()
+    doc = {"bundles": [bench.PO2_BUNDLE.name, bench.DB_BUNDLE.name, bench.LOGRANDOM_BUNDLE.name],
            "probe_shapes": [list(p) for p in probes],
            "po2": pipeline_doc(po2, "po2", probes),
-           "hybrid": pipeline_doc(hybrid, "hybrid", probes)}
+           "hybrid": pipeline_doc(hybrid, "hybrid", probes),
+           "headline": pipeline_doc(headline, "hybrid", probes)}
     (HERE / "b200_trees.json").write_text(json.dumps(doc, separators=(",", ":")))
     print("wrote", HERE / "b200_trees.json")
 

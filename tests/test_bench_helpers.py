@@ -46,15 +46,20 @@ def test_x3_tables_merge_every_shape_with_fp32_rows_first():
         assert t.peak_gflops == max(m.gflops for m in t.measurements)
 
 
-def test_headline_model_trains_on_po2_tables_only():
-    """The headline tree sees po2 tables only: every training shape is a
-    power of two in each dimension; the DeepBench shapes that are not po2
-    grid points (32 of 40) are never seen, and the bench reports them
-    separately (dt_vs.unseen)."""
+def test_headline_model_trains_on_generated_shapes_only():
+    """The headline tree sees the po2 and octave-uniform random tables only
+    (no DeepBench table): its training set is the CLI hybrid of the two
+    sweeps, one seeded split; the DeepBench shapes that are not training
+    shapes are reported separately (dt_vs.unseen)."""
+    from paper_1806_07060_b200.dataset import gen_po2, gen_random
     from paper_1806_07060_b200.tuner import load_table_bundle
-    pipe = bench._pipeline(load_table_bundle(bench.PO2_BUNDLE), "po2")
-    pow2 = lambda v: v & (v - 1) == 0  # noqa: E731
-    assert len(pipe["train"]) == 583 and all(pow2(x) for mnk in pipe["train"] for x in mnk)
+    po2, tables = bench.training_tables()
+    gen = [s.mnk for s in gen_po2(16, 4096)] + [s.mnk for s in gen_random(512, 16, 4096, 2026, "log2")]
+    assert [t.shape.mnk for t in tables] == list(dict.fromkeys(gen))
+    assert [t.shape.mnk for t in po2] == [s.mnk for s in gen_po2(16, 4096)]
+    pipe = bench._pipeline(tables, "hybrid")
+    assert pipe["n_train"] == int(0.8 * len(tables))
     db = {t.shape.mnk for t in load_table_bundle(bench.DB_BUNDLE)}
+    pow2 = lambda v: v & (v - 1) == 0  # noqa: E731
     off_grid = {mnk for mnk in db if not all(pow2(x) for x in mnk)}
     assert len(off_grid) == 32 and not off_grid & pipe["train"]

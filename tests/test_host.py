@@ -582,6 +582,33 @@ def test_gen_random_shapes_deterministic_and_in_range():
         gen_random(9, 1, 2, 0)
 
 
+def test_gen_random_log2_octave_uniform():
+    from paper_1806_07060_b200.dataset import gen_random
+    a = gen_random(512, 16, 4096, 2026, "log2")
+    assert [s.mnk for s in a] == [s.mnk for s in gen_random(512, 16, 4096, 2026, "log2")]
+    assert len({s.mnk for s in a}) == 512
+    assert all(16 <= d < 4096 for s in a for d in s.mnk)
+    # first draw: an octave index, then an offset inside the octave
+    g = rng.SplitMix64(2026)
+    first = []
+    for _ in range(3):
+        base = 16 << g.below(8)
+        first.append(base + g.below(base))
+    assert a[0].mnk == tuple(first)
+    # every octave of [16, 4096) is populated in every dimension
+    for dim in range(3):
+        assert {s.mnk[dim].bit_length() for s in a} == set(range(5, 13))
+    with pytest.raises(ValueError):
+        gen_random(8, 16, 1000, 0, "log2")
+    with pytest.raises(ValueError):
+        gen_random(8, 16, 1024, 0, "gauss")
+    # the sweep config that produced tables_b200_lograndom.csv.gz
+    from paper_1806_07060_b200 import cli
+    cfg = cli.PipelineConfig.load(ROOT / "configs" / "lograndom_b200.json")
+    shapes, tag = cfg.shapes()
+    assert tag == "random" and [s.mnk for s in shapes] == [s.mnk for s in a]
+
+
 def test_sampling_list_configs_and_tc_config_file():
     from paper_1806_07060_b200 import cli
     from paper_1806_07060_b200.kernels import KernelFamily, enumerate_search_space
@@ -627,14 +654,12 @@ def test_shipped_b200_models_match_reference():
     doc = json.loads(path.read_text())
     po2 = load_table_bundle(bench.PO2_BUNDLE)
     db = load_table_bundle(bench.DB_BUNDLE)
-    assert doc["bundles"] == [bench.PO2_BUNDLE.name, bench.DB_BUNDLE.name]
-    hybrid, seen = [], set()
-    for t in po2 + db:
-        if t.shape.mnk not in seen:
-            seen.add(t.shape.mnk)
-            hybrid.append(t)
+    assert doc["bundles"] == [bench.PO2_BUNDLE.name, bench.DB_BUNDLE.name, bench.LOGRANDOM_BUNDLE.name]
+    hybrid = bench.dedup_tables(po2 + db)
+    _, headline = bench.training_tables()
     probes = [tuple(p) for p in doc["probe_shapes"]]
-    for key, tables, prov in (("po2", po2, "po2"), ("hybrid", hybrid, "hybrid")):
+    for key, tables, prov in (("po2", po2, "po2"), ("hybrid", hybrid, "hybrid"),
+                              ("headline", headline, "hybrid")):
         want = doc[key]
         ds = dataset_from_tables(tables, prov)
         recs = ds.features_and_labels()
