@@ -279,7 +279,8 @@ ag_selector* ag_selector_build_kind(const int32_t* node_feature, const double* n
 void ag_selector_free(ag_selector* sel);
 /* 0 = bucket table, 1 = predicated walk */
 int ag_selector_kind(const ag_selector* sel);
-/* the selected leaf: its class id is returned, its config copied out */
+/* the selected leaf: its class id is returned, its config copied out
+   (-1 and ag_last_error set for a null selector) */
 int64_t ag_select(const ag_selector* sel, int64_t m, int64_t n, int64_t k, ag_config* out);
 /* batched select; returns class ids for n_queries (m,n,k) triples */
 int ag_select_many(const ag_selector* sel, const int64_t* mnk, int64_t n_queries,

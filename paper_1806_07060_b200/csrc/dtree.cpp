@@ -181,6 +181,11 @@ const int64_t kTableCap = 1 << 18;  // 1 MB of int32 leaf ids
 
 }  // namespace
 
+namespace ag {
+int set_last_error(int code, const std::string& msg);
+std::string config_string(const ag_config& c);
+}  // namespace ag
+
 extern "C" {
 
 int ag_best_split(const int64_t* features, const int64_t* labels, int64_t n_records, int64_t min_leaf,
@@ -362,13 +367,14 @@ void ag_selector_free(ag_selector* s) { delete s; }
 int ag_selector_kind(const ag_selector* s) { return s ? s->kind : -1; }
 
 int64_t ag_select(const ag_selector* s, int64_t m, int64_t n, int64_t k, ag_config* out) {
+    if (!s) return ag::set_last_error(AG_ERR_CONFIG, "null selector"), -1;
     const int64_t i = leaf_of(s, m, n, k);
     if (out) *out = s->cfg[i];
     return s->cls[i];
 }
 
 int ag_select_many(const ag_selector* s, const int64_t* mnk, int64_t n_queries, int64_t* class_ids) {
-    if (!s) return AG_ERR_CONFIG;
+    if (!s) return ag::set_last_error(AG_ERR_CONFIG, "null selector");
     for (int64_t q = 0; q < n_queries; ++q) class_ids[q] = s->cls[leaf_of(s, mnk[3 * q], mnk[3 * q + 1], mnk[3 * q + 2])];
     return AG_OK;
 }
@@ -385,11 +391,6 @@ double ag_select_bench_ns(const ag_selector* s, int64_t m, int64_t n, int64_t k,
 }
 
 }  // extern "C"
-
-namespace ag {
-int set_last_error(int code, const std::string& msg);
-std::string config_string(const ag_config& c);
-}  // namespace ag
 
 namespace {
 // the tree's pick, or the fallback when the pick is illegal under `caps` or

@@ -157,3 +157,16 @@ def test_host_scratch_bytes():
     d = KernelConfig(KernelFamily.DIRECT, 16, 16, 8, 2, 2, 1)
     assert lib.ag_host_scratch_bytes(ctypes.byref(s), ctypes.byref(d.native()), 0, 1) == \
         up(1000 * 50 * 4) + up(50 * 300 * 4) + 2 * up(1000 * 300 * 4)
+
+
+def test_null_selector_reports_an_error():
+    """ag_select / ag_select_many on a null selector fail with AG_ERR_CONFIG
+    and a message (no stale or empty ag_last_error)."""
+    lib = _native.lib()
+    cfg = _native.AgConfig()
+    assert lib.ag_select(None, 64, 64, 64, ctypes.byref(cfg)) == -1
+    assert b"null selector" in lib.ag_last_error()
+    mnk = (ctypes.c_int64 * 3)(64, 64, 64)
+    ids = (ctypes.c_int64 * 1)()
+    assert lib.ag_select_many(None, mnk, 1, ids) != 0
+    assert b"null selector" in lib.ag_last_error()
