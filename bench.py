@@ -54,6 +54,7 @@ LOGRANDOM_BUNDLE = DATA / "tables_b200_lograndom.csv.gz"
 # merged per shape into the fp32 tables by x3_section
 X3_PO2_BUNDLE = DATA / "tables_x3_po2.csv.gz"
 X3_DB_BUNDLE = DATA / "tables_x3_deepbench.csv.gz"
+X3_LOGRANDOM_BUNDLE = DATA / "tables_x3_lograndom.csv.gz"
 TRAFFIC_FILE = ROOT / "profiles" / "roofline_traffic.json"
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -887,15 +888,18 @@ def tc_section(m, policy, device, distributed, times, fallback, args):
 
 
 def load_x3_tables():
-    """(po2, DeepBench) tables of the fp32 space with the tf32x3 rows of the
-    same shapes merged in (tuner.merge_tables: fp32 rows first)."""
+    """(training, DeepBench) tables of the fp32 space with the tf32x3 rows of
+    the same shapes merged in (tuner.merge_tables: fp32 rows first).  The
+    training tables are the headline's training set (po2 + the octave-uniform
+    random shapes, deduplicated in order)."""
     from paper_1806_07060_b200.tuner import load_table_bundle, merge_tables
 
     def merged(base, extra):
         by = {t.shape.mnk: t for t in load_table_bundle(extra)}
         return [merge_tables(t, by[t.shape.mnk]) for t in load_table_bundle(base)]
 
-    return merged(PO2_BUNDLE, X3_PO2_BUNDLE), merged(DB_BUNDLE, X3_DB_BUNDLE)
+    train = dedup_tables(merged(PO2_BUNDLE, X3_PO2_BUNDLE) + merged(LOGRANDOM_BUNDLE, X3_LOGRANDOM_BUNDLE))
+    return train, merged(DB_BUNDLE, X3_DB_BUNDLE)
 
 
 # The bench regime's streaming-read floor (profiles/r02_read_floor.jsonl,
@@ -925,8 +929,8 @@ def regime_floor_s(shape, ffma_tflops):
 
 def x3_section(cases, default_t, device, distributed, times, fallback, args):
     """The fp32 space plus tf32x3 (fp32-accurate 3xTF32 on tcgen05, RF <=
-    1e-5 like the fp32 families): the reference pipeline on the merged po2
-    tables (no DeepBench table in training), the DT measured live on the
+    1e-5 like the fp32 families): the reference pipeline on the merged
+    po2 + random tables (no DeepBench table in training), the DT measured live on the
     DeepBench set against the merged oracle and the fp32 default tile; the
     whole output of the largest tf32x3 pick checked against the float64
     product; roofline of the dominant tf32x3 kernel against tf32 peak / 3."""
@@ -934,11 +938,12 @@ def x3_section(cases, default_t, device, distributed, times, fallback, args):
 
     from paper_1806_07060_b200 import codegen
     from paper_1806_07060_b200.kernels import DeviceCaps, KernelFamily
-    if not X3_PO2_BUNDLE.exists() or not X3_DB_BUNDLE.exists():
-        return {"unavailable": f"no {X3_PO2_BUNDLE.name} / {X3_DB_BUNDLE.name}"}
-    po2, db_list = load_x3_tables()
+    missing = [b.name for b in (X3_PO2_BUNDLE, X3_DB_BUNDLE, X3_LOGRANDOM_BUNDLE) if not b.exists()]
+    if missing:
+        return {"unavailable": f"no {' / '.join(missing)}"}
+    train, db_list = load_x3_tables()
     db = {t.shape.mnk: t for t in db_list}
-    pipe = _pipeline(po2, "po2")
+    pipe = _pipeline(train, "hybrid")
     sel = codegen.CompiledSelector(pipe["tree"], pipe["classes"])
     runner = Runner(device, DeviceCaps.b200_tc())
     reps = max(4, args.steps // 2)

@@ -36,9 +36,10 @@ def test_pack_launches_per_family(canon, shape, n):
 
 
 def test_x3_tables_merge_every_shape_with_fp32_rows_first():
-    po2, db = bench.load_x3_tables()
-    assert len(po2) == 729 and len(db) == 40
-    for t in db:
+    train, db = bench.load_x3_tables()
+    assert len(train) == 729 + 512 and len(db) == 40
+    assert [t.shape.mnk for t in train] == [t.shape.mnk for t in bench.training_tables()[1]]
+    for t in db + train[::97]:
         fams = [m.config.family for m in t.measurements]
         first_x3 = fams.index(KernelFamily.TF32X3)
         assert all(f is not KernelFamily.TF32X3 for f in fams[:first_x3])

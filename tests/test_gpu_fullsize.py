@@ -131,12 +131,12 @@ def test_fp64_blas_matches_reference_oracle(mnk):
 
 def test_x3_deepbench_all_picks_full_size():
     """The fp32 space + tf32x3 (bench.py fp32_accurate_tc): the tree the
-    reference pipeline trains on the merged po2 tables, its pick, the merged
-    oracle and the default on every DeepBench shape, whole output vs the
-    float64 product at the fp32 bar (1e-5) -- tf32x3 included."""
+    reference pipeline trains on the merged po2 + random tables, its pick,
+    the merged oracle and the default on every DeepBench shape, whole output
+    vs the float64 product at the fp32 bar (1e-5) -- tf32x3 included."""
     import bench
-    po2, db = bench.load_x3_tables()
-    pipe = bench._pipeline(po2, "po2")
+    train, db = bench.load_x3_tables()
+    pipe = bench._pipeline(train, "hybrid")
     sel = codegen.CompiledSelector(pipe["tree"], pipe["classes"])
     fams = set()
     worst = _check([t.shape for t in db], sel, {t.shape.mnk: t for t in db}, pipe["policy"], DeviceCaps.b200_tc(),
