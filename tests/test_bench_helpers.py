@@ -64,3 +64,39 @@ def test_headline_model_trains_on_generated_shapes_only():
     pow2 = lambda v: v & (v - 1) == 0  # noqa: E731
     off_grid = {mnk for mnk in db if not all(pow2(x) for x in mnk)}
     assert len(off_grid) == 32 and not off_grid & pipe["train"]
+
+def test_headline_training_set_is_a_cli_hybrid_config():
+    """configs/headline_b200.json reproduces the headline training set through
+    the reference-compatible CLI (tune / dataset / train): its hybrid dataset
+    lists exactly the shapes of bench.training_tables(), in order."""
+    from paper_1806_07060_b200 import cli
+    cfg = cli.PipelineConfig.load(bench.ROOT / "configs" / "headline_b200.json")
+    shapes, tag = cfg.shapes()
+    assert tag == "hybrid" and cfg.caps.profile == "b200"
+    assert [s.mnk for s in shapes] == [t.shape.mnk for t in bench.training_tables()[1]]
+
+
+def test_headline_cli_stages_pick_the_bench_tree(tmp_path):
+    """The CLI's dataset / train / eval stages on the shipped tables of
+    configs/headline_b200.json (written where `tune` would put them) choose
+    the same model, with the same tree, as bench.build_model()."""
+    import json
+
+    from paper_1806_07060_b200 import cli, codegen, model
+    from paper_1806_07060_b200.tuner import save_table, table_filename
+    doc = json.loads((bench.ROOT / "configs" / "headline_b200.json").read_text())
+    doc["out_dir"] = str(tmp_path / "out")
+    path = tmp_path / "headline.json"
+    path.write_text(json.dumps(doc))
+    cfg = cli.PipelineConfig.load(path)
+    cfg.tables_dir.mkdir(parents=True)
+    for t in bench.training_tables()[1]:
+        save_table(t, cfg.tables_dir / table_filename(t.shape), {"config_hash": cfg.hash()})
+    for stage in ("dataset", "train", "eval"):
+        assert cli.main([stage, "--config", str(path)]) == 0
+    best = json.loads((cfg.out / "best_model.json").read_text())
+    m = bench.build_model()
+    assert best["name"] == m["name"]
+    cli_tree = model.load_tree(best["path"])
+    assert cli_tree.meta.pop("config_hash") == cfg.hash()  # the CLI stamps its config; otherwise equal
+    assert codegen.tree_fingerprint(cli_tree) == codegen.tree_fingerprint(m["tree"])
