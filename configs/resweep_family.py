@@ -9,6 +9,10 @@ policy on resident buffers, then write the shape's table with those rows
 replaced (tuner.merge_tables, the re-timed rows win) in the full enumeration
 order.  Used after a kernel change that touches one family only (the
 split-K in-place core), so the other families' measurements are kept.
+`--odd-n-only`: only shapes with N % 4 != 0 (the in-place core's element
+copies of B, round 2) are re-timed.
+
+    python configs/resweep_family.py --unbundle BUNDLE.csv.gz TABLES_DIR
 """
 import argparse
 import sys
@@ -26,11 +30,20 @@ from paper_1806_07060_b200.tuner import load_table, merge_tables, save_table, ta
 
 
 def main():
+    if len(sys.argv) == 4 and sys.argv[1] == "--unbundle":  # a shipped bundle -> per-shape tables
+        from paper_1806_07060_b200.tuner import load_table_bundle
+        out = Path(sys.argv[3])
+        out.mkdir(parents=True, exist_ok=True)
+        for t in load_table_bundle(sys.argv[2]):
+            save_table(t, out / table_filename(t.shape))
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("family")
     ap.add_argument("config")
     ap.add_argument("old")
     ap.add_argument("new")
+    ap.add_argument("--odd-n-only", action="store_true",
+                    help="re-time only shapes whose N is not a multiple of 4 (the others are copied)")
     a = ap.parse_args()
     cfg = cli.PipelineConfig.load(a.config)
     shapes, _ = cfg.shapes()
@@ -48,6 +61,9 @@ def main():
         if dst.exists():
             continue
         old = load_table(Path(a.old) / table_filename(s))
+        if a.odd_n_only and s.N % 4 == 0:
+            save_table(old, dst)
+            continue
         fresh = tune_configs(s, mine, cfg.caps, cfg.timing)
         merged = merge_tables(fresh, old, order)
         merged.meta.update({k: v for k, v in old.meta.items() if k not in ("configs",)})
