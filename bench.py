@@ -11,15 +11,18 @@ reported beside it.
 
 The tree is the reference pipeline's (dataset -> seeded 80/20 split ->
 5x8 CART grid -> best test DTPR) trained on the exhaustive B200 tuning
-tables shipped in paper_1806_07060_b200/data/ (produced on a B200 by
-`python -m paper_1806_07060_b200.cli tune`, see configs/).  The oracle and
-default configs come from those tables; all three are re-measured live.
+tables of generated shape sets shipped in paper_1806_07060_b200/data/ (po2
+16..4096 + 512 octave-uniform random shapes, configs/headline_b200.json;
+produced on a B200 by `python -m paper_1806_07060_b200.cli tune`).  No
+DeepBench table is used in training or model selection; the DeepBench
+tables give the oracle and the default configs; all three are re-measured
+live.
 
 One step = one pass over the shape set: per shape, L2 flushed (256 MB
 write), then the DT path -- native branch-free select + launch through the
 C-ABI (ag_dispatch_gemm) on operands resident in HBM -- bracketed by CUDA
 events on the launching stream.  value = geomean over shapes of
-2MNK / median event time.  e2e = the same metric through the public Python
+2MNK / trimmed-mean event time.  e2e = the same metric through the public Python
 API with host (numpy) buffers, host<->device copies inside the timed call.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
