@@ -14,9 +14,9 @@ The tree is the reference pipeline's (dataset -> seeded 80/20 split ->
 tables of generated shape sets shipped in paper_1806_07060_b200/data/ (po2
 16..4096 + 512 octave-uniform random shapes, configs/headline_b200.json;
 produced on a B200 by `python -m paper_1806_07060_b200.cli tune`).  No
-DeepBench table is used in training or model selection; the DeepBench
-tables give the oracle and the default configs; all three are re-measured
-live.
+DeepBench table is used in training or model selection.  The DeepBench
+tables give the oracle per shape; the default tile is the BaselinePolicy
+anchored on the 256^3 / 1024^3 po2 tables; all three are re-measured live.
 
 One step = one pass over the shape set: per shape, L2 flushed (256 MB
 write), then the DT path -- native branch-free select + launch through the
