@@ -345,7 +345,11 @@ def pack_launches(shape, cfg) -> int:
     arow_fit = not shape.transA and shape.M % cfg.block_m == 0 and shape.K % cfg.block_k == 0
     if (cfg.family is KernelFamily.SPLITK and not shape.transA and not shape.transB and shape.K % 4 == 0
             and shape.N % 4 == 0 and (shape.N <= 64 or not arow_fit)):
-        return 1  # in-place core, slices reduced inside the cluster (no packs, no reduce launch)
+        ktiles = -(-shape.K // cfg.block_k)
+        kps = -(-ktiles // cfg.unroll_k)
+        # in-place core; up to 8 slices reduce inside the cluster, more take
+        # the slab + reduce launch (launch.cuh launch_inplace)
+        return 1 if -(-ktiles // kps) <= 8 else 2
     n = 1
     a_in_place = (shape.transA and shape.M % cfg.block_m == 0 and shape.K % cfg.block_k == 0) or \
         (cfg.family is KernelFamily.SPLITK and arow_fit)

@@ -9,6 +9,7 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <type_traits>
@@ -225,7 +226,19 @@ int launch_inplace(const GemmCall& c) {
 #ifdef AG_NO_CLUSTER_REDUCE  // measurement knob (profiles/exp_tiles.cu): slab + reduce kernel only
     if (false) {
 #else
-    if (used_splits > 1 && used_splits <= 16) {
+    // AG_SPLITK_REDUCE=slab (measurement knob, profiles/reduce_mode_probe.py):
+    // the slab + splitk_reduce_kernel path even where a cluster fits
+    static const bool force_slab = [] {
+        const char* e = std::getenv("AG_SPLITK_REDUCE");
+        return e && std::string(e) == "slab";
+    }();
+    // Clusters of up to 8 slices (the portable size).  More slices take the
+    // slab path: a 16-CTA non-portable cluster must be co-resident in one
+    // GPC.  Over the 1200 (DeepBench shape, config) calls with > 8 slices the
+    // slab path is 1.12x faster (geomean; median 1.13x, p10 1.00x, min
+    // 0.90x); with 2..8 slices the two are even (1.007x) and the single
+    // launch is kept (profiles/r02_reduce_mode_probe.jsonl).
+    if (used_splits > 1 && used_splits <= 8 && !force_slab) {
 #endif
         static PerDevice<int> np_ok_dev;
         std::atomic<int>& np_ok = np_ok_dev.here();

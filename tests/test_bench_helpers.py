@@ -31,6 +31,8 @@ def test_regime_floor_is_the_slower_of_compute_and_read():
     ("skinny_n:64-16-32-2-4-4", (2048, 16, 2048), 1),
     ("direct:16-16-8-2-2-1", (64, 64, 64), 1),
     ("splitk:64-128-32-8-8-4", (5124, 700, 2048), 1),  # in-place core, cluster reduction
+    ("splitk:32-64-16-4-4-16", (35, 1500, 2560), 2),  # 16 slices: in-place core + slab reduction
+    ("splitk:16-16-32-2-2-16", (64, 16, 64), 1),  # 16-slice config, 2 K tiles: 2 slices, cluster
     # N = 8457 is not a multiple of 4: pack A, pack-pad B, core, slab reduction
     # (the four launches of profiles/r02_splitk_packed_35x8457x2560.json)
     ("splitk:32-64-16-4-4-16", (35, 8457, 2560), 4),

@@ -101,7 +101,7 @@ def test_tc_held_out_all_picks_full_size(shipped):
 
 @pytest.mark.parametrize("mnk,canon", [
     ((2048, 16, 2048), "splitk:32-16-32-4-2-8"),      # in-place core, 8-slice cluster (DSMEM) reduction
-    ((2048, 128, 2048), "splitk:128-128-32-8-8-16"),  # 16-slice non-portable cluster
+    ((2048, 128, 2048), "splitk:128-128-32-8-8-16"),  # 16 slices: in-place core + slab reduction
     ((7680, 128, 2560), "splitk:64-128-16-8-8-16"),
     ((35, 8457, 2560), "splitk:64-128-32-8-8-8"),     # N % 4 != 0: packed core + splitk_reduce_kernel
     ((4096, 16, 4096), "splitk:32-16-32-4-2-16"),
